@@ -1,0 +1,147 @@
+/*
+ * isort.h -- C ABI of the B200-native integer-sort engine (libisort.so).
+ *
+ * Drop-in boundary for the reference's sort path (arxiv 1206.3511,
+ * /root/reference/proj).  The reference's public entry points live in
+ * proj/core/include/intsort/sort.hpp and are bound to the harness through
+ * SortFn / make_sort_fn (proj/core/include/intsort/bench.hpp:44-49).  Each
+ * group below names the reference interface it replaces.  A C++ adapter with
+ * the unchanged signatures (paper_1206_3511_b200/dropin/sort_b200.cpp) sits on
+ * top; INTEGRATION.md shows how a maintainer swaps it in for sort.cpp.
+ *
+ * Conventions
+ *  - All functions return ISORT_OK (0) or an ISORT_E* code; the message is in
+ *    isort_last_error() (thread-local).  Argument errors that the reference
+ *    reports with std::invalid_argument return ISORT_EINVAL with the
+ *    reference's wording.
+ *  - "Device" entry points take device pointers, a caller-provided temp
+ *    buffer (size from the matching *_temp_bytes) and a cudaStream_t passed
+ *    as void*.  They are asynchronous: no host synchronisation, except where
+ *    noted (bucket sort reads back one small status word).
+ *  - "Host" entry points take host pointers, own their device memory and
+ *    synchronise before returning (the reference is synchronous).
+ *  - There is no CPU fallback: without a usable CUDA device every call
+ *    returns ISORT_ECUDA.
+ */
+#ifndef ISORT_H
+#define ISORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISORT_OK 0
+#define ISORT_ENOMEM 12
+#define ISORT_EINVAL 22  /* reference: std::invalid_argument */
+#define ISORT_ERANGE 34  /* n beyond the engine's per-call limit (2^30 - 1 keys) */
+#define ISORT_ECUDA 1001
+#define ISORT_ENCCL 1002
+
+#define ISORT_ABI_VERSION 1
+
+/* Layout-compatible with intsort::Record {Key key; uint64_t tag;}
+ * (proj/core/include/intsort/record.hpp:20-25). */
+typedef struct isort_record {
+    uint64_t key;
+    uint64_t tag;
+} isort_record;
+
+/* Payload handling for the device sorts. */
+enum isort_vals_mode {
+    ISORT_VALS_NONE = 0, /* keys only */
+    ISORT_VALS_LOAD = 1, /* vals_in[] carried along (u32 payload) */
+    ISORT_VALS_IOTA = 2  /* payload = original position, generated on device */
+};
+
+const char* isort_last_error(void);
+int isort_abi_version(void);
+/* Largest n one device call accepts. */
+uint64_t isort_max_keys(void);
+/* Bad input index of the last ISORT_EINVAL range failure (UINT64_MAX if none). */
+uint64_t isort_last_bad_index(void);
+
+/* Observability (used by bench.py).  isort_launch_count: kernels this library
+ * has launched so far in the process.  isort_profile_begin/end: record a CUDA
+ * event on the launching stream after every phase (memset, upfront, plan,
+ * pass0..7, copy, windows, resolve, fallback) of the calls made in between on
+ * this thread; end() synchronises, writes per-phase milliseconds and
+ * NUL-terminated phase names (names_stride bytes each), the number of phases,
+ * and the number of digit passes the last pipeline actually executed. */
+uint64_t isort_launch_count(void);
+int isort_profile_begin(void);
+int isort_profile_end(float* ms, char* names, int names_stride, int max_phases, int* count,
+                      int* n_active);
+
+/* ------------------------------------------------------------------------
+ * LSD radix sort, device-resident.
+ * Replaces: intsort::radix_sort_lsd(const RecordSeq&, uint64_t base)
+ *           (sort.hpp:37-40, sort.cpp:112-119) and the build_radix_plan /
+ *           counting_sort_by_digit chain it runs (sort.cpp:57-110).
+ * Stable; output identical for every base >= 2 (test_sort.cpp:136-149), so
+ * the device sorts with 8-bit digits and skips digit passes that are the
+ * identity.  keys_in is not modified; keys_out receives the sorted keys.
+ * ---------------------------------------------------------------------- */
+size_t isort_radix_temp_bytes(uint64_t n, int key_bytes, int vals_mode);
+int isort_radix_sort_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                         uint32_t* vals_out, uint64_t n, int vals_mode, void* temp,
+                         size_t temp_bytes, void* stream);
+int isort_radix_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
+                         uint32_t* vals_out, uint64_t n, int vals_mode, void* temp,
+                         size_t temp_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Bucket sort, device-resident.
+ * Replaces: intsort::bucket_sort(const RecordSeq&, Key range_bound)
+ *           (sort.hpp:50-53, sort.cpp:136-152) with bucket_index
+ *           (sort.cpp:121-134): n buckets, b = floor(n*key/(M+1)).
+ * A key > range_bound returns ISORT_EINVAL with the reference's message for
+ * the first offending input position (isort_last_bad_index()).  This call
+ * synchronises `stream` once to read that status.
+ * ---------------------------------------------------------------------- */
+size_t isort_bucket_temp_bytes(uint64_t n, int key_bytes, int vals_mode);
+int isort_bucket_sort_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                          uint32_t* vals_out, uint64_t n, uint64_t range_bound, int vals_mode,
+                          void* temp, size_t temp_bytes, void* stream);
+int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
+                          uint32_t* vals_out, uint64_t n, uint64_t range_bound, int vals_mode,
+                          void* temp, size_t temp_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Host-memory entry points: the drop-in path (H2D, sort, D2H inside).
+ * ---------------------------------------------------------------------- */
+/* radix_sort_lsd(input, base): sort.hpp:40. */
+int isort_radix_sort_records(const isort_record* in, isort_record* out, uint64_t n,
+                             uint64_t base, int device);
+/* bucket_sort(input, range_bound): sort.hpp:53. */
+int isort_bucket_sort_records(const isort_record* in, isort_record* out, uint64_t n,
+                              uint64_t range_bound, int device);
+/* counting_sort_by_digit(input, RadixPlan{base, digits}, digit_index): sort.hpp:30-35. */
+int isort_counting_sort_by_digit_records(const isort_record* in, isort_record* out, uint64_t n,
+                                         uint64_t base, uint32_t digits, uint32_t digit_index,
+                                         int device);
+/* build_radix_plan(input, base).digits: sort.hpp:28. */
+int isort_build_radix_plan_records(const isort_record* in, uint64_t n, uint64_t base,
+                                   uint32_t* digits, int device);
+/* Keys-only u32 through host buffers (the end-to-end benchmark call). */
+int isort_radix_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n, int device);
+int isort_bucket_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n,
+                               uint64_t range_bound, int device);
+
+/* Device batch of bucket_index (sort.hpp:42-48, sort.cpp:121-134): out[i] =
+ * floor(bucket_count * keys[i] / (range_bound + 1)) with the exact 128-bit
+ * semantics, or UINT64_MAX where keys[i] > range_bound.  ISORT_EINVAL when
+ * bucket_count == 0.  Device pointers; asynchronous on `stream`. */
+int isort_bucket_index_u64(const uint64_t* keys, uint64_t* out, uint64_t m, uint64_t bucket_count,
+                           uint64_t range_bound, void* stream);
+
+/* Device-side is_sorted (verify.hpp:12-13) over u32 keys: *result = 1/0. */
+int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ISORT_H */

@@ -1,0 +1,73 @@
+"""In-tree build of the engine (and of the parity checker under oracle/).
+
+* ``libisort.so``: every CUDA source in csrc/ compiled for sm_100a only
+  (``-gencode arch=compute_100a,code=sm_100a``), ``-lineinfo`` so ncu's source
+  page maps to our code.  Built next to this file so it travels to the GPU box
+  with the repo snapshot.
+* ``oracle/liboracle.so`` (the C restatement) and, where /root/reference
+  exists, ``oracle/_ref/*`` (the reference itself) -- test infrastructure only.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libisort.so")
+REFERENCE = "/root/reference/proj"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O3", "-shared",
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build the sm_100a engine (no CPU fallback exists)")
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_engine(force: bool = False, verbose: bool = False) -> str:
+    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                     + [os.path.join(ROOT, "include", "isort.h")])
+    if force or _stale(LIB, sources):
+        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "isort_api.cu")]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """Build the checker: our restatement always, the reference where it exists."""
+    oracle = os.path.join(ROOT, "oracle")
+    targets = ["oracle"]
+    if os.path.isdir(REFERENCE):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", oracle, *targets], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_engine(force=force, verbose=verbose)
+    build_oracle(verbose=verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

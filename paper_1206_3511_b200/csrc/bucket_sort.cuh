@@ -1,0 +1,466 @@
+// bucket_sort.cuh -- bucket sort (n buckets over [0, M]) for sm_100a.
+//
+// Reference semantics: intsort::bucket_sort (proj/core/src/sort.cpp:136-152):
+// n buckets, record r goes to bucket_index(r.key, n, M) = floor(n*key/(M+1))
+// (sort.cpp:121-134, 128-bit product), arrival order kept inside a bucket,
+// each bucket insertion-sorted (stable, sort.cpp:15-25), buckets concatenated.
+// The result is the unique stable sort by key; a key > M throws
+// std::invalid_argument naming that key (sort.cpp:125-129).
+//
+// Device pipeline:
+//   K1  k_upfront (shared with radix) with BucketDigitizer: range check (first
+//       offending position), sortedness, histograms of the top 8-bit digits of
+//       the bucket index b.                                            4n B
+//   K3  D_b stable one-sweep passes (low digit first) scatter the keys into
+//       contiguous super-buckets: runs of 2^s_lo consecutive buckets (the top
+//       8*D_b bits of b), bucket order, arrival order kept.    D_b x 8n B
+//       D_b = ceil((L - 11) / 8) for L = bits(n - 1): a super-bucket covers
+//       <= 2^11 buckets (~2K keys on average).
+//   K5  k_bucket_windows: each CTA owns the super-buckets that START in its
+//       window, stages them (plus up to kCap keys of overhang) in shared memory
+//       and sorts them stably by key.  A stable sort of whole buckets laid out
+//       in bucket order equals per-bucket insertion sort + concatenation,
+//       because bucket_index is monotone in the key.                    8n B
+//   K6  k_resolve_oversized: a super-bucket longer than a window's reach is
+//       resolved from per-window summaries (boundary, min, max); one that
+//       holds a single key value is already in arrival order, the others mark
+//       a span that the radix pipeline re-sorts ("oversized buckets go to the
+//       radix kernel").
+#pragma once
+
+#include "isort_common.cuh"
+#include "radix_onesweep.cuh"
+
+namespace isort {
+
+// ------------------------------------------------------ bucket index
+// b(key) = floor(count * key / (M + 1)) exactly as bucket_index computes it
+// with unsigned __int128 (sort.cpp:131-133).
+struct BucketIndexer {
+    uint64_t count;       // number of buckets (= n)
+    uint64_t bound;       // M (inclusive range bound)
+    uint64_t div;         // M + 1 when it fits in 64 bits
+    uint64_t magic;       // floor((2^64 - 1) / div), general path
+    uint32_t pow2_shift;  // M + 1 == 2^pow2_shift (0..64), 255 otherwise
+
+    static BucketIndexer make(uint64_t count, uint64_t bound) {
+        BucketIndexer b{};
+        b.count = count;
+        b.bound = bound;
+        if (bound == ~0ull) {
+            b.pow2_shift = 64;
+        } else {
+            b.div = bound + 1;
+            if ((b.div & (b.div - 1)) == 0) {
+                b.pow2_shift = static_cast<uint32_t>(__builtin_ctzll(b.div));
+            } else {
+                b.pow2_shift = 255;
+                b.magic = ~0ull / b.div;
+            }
+        }
+        return b;
+    }
+
+    // Keys above M are clamped into the last bucket so the device passes stay
+    // in bounds; k_upfront's range check reports them.
+    __host__ __device__ __forceinline__ uint64_t bucket(uint64_t key) const {
+        if (key > bound) return count - 1;
+#ifdef __CUDA_ARCH__
+        const uint64_t hi = __umul64hi(count, key);
+#else
+        const uint64_t hi = static_cast<uint64_t>((static_cast<unsigned __int128>(count) * key) >> 64);
+#endif
+        const uint64_t lo = count * key;
+        if (pow2_shift != 255) {
+            if (pow2_shift == 64) return hi;
+            if (pow2_shift == 0) return lo;
+            return (lo >> pow2_shift) | (hi << (64 - pow2_shift));
+        }
+        if (hi == 0) {
+#ifdef __CUDA_ARCH__
+            uint64_t q = __umul64hi(lo, magic);  // floor(lo/div) - 2 <= q <= floor(lo/div)
+#else
+            uint64_t q = static_cast<uint64_t>((static_cast<unsigned __int128>(lo) * magic) >> 64);
+#endif
+            uint64_t r = lo - q * div;
+            while (r >= div) {
+                ++q;
+                r -= div;
+            }
+            return q;
+        }
+        // 128-by-64 division; the quotient is < count because key <= M.
+        // Floating estimate, then exact integer correction.
+        const double approx = (static_cast<double>(hi) * 18446744073709551616.0 + static_cast<double>(lo)) /
+                              static_cast<double>(div);
+        uint64_t q = approx <= 0.0 ? 0ull : (approx >= 1.8e19 ? count - 1 : static_cast<uint64_t>(approx));
+        if (q >= count) q = count - 1;
+        for (;;) {  // while q*div > p: --q
+#ifdef __CUDA_ARCH__
+            const uint64_t phi = __umul64hi(q, div);
+#else
+            const uint64_t phi = static_cast<uint64_t>((static_cast<unsigned __int128>(q) * div) >> 64);
+#endif
+            const uint64_t plo = q * div;
+            if (phi > hi || (phi == hi && plo > lo)) {
+                --q;
+                continue;
+            }
+            break;
+        }
+        for (;;) {  // while (q+1)*div <= p: ++q
+            const uint64_t q1 = q + 1;
+#ifdef __CUDA_ARCH__
+            const uint64_t phi = __umul64hi(q1, div);
+#else
+            const uint64_t phi = static_cast<uint64_t>((static_cast<unsigned __int128>(q1) * div) >> 64);
+#endif
+            const uint64_t plo = q1 * div;
+            if (phi < hi || (phi == hi && plo <= lo)) {
+                q = q1;
+                continue;
+            }
+            break;
+        }
+        return q;
+    }
+};
+
+constexpr int kBucketMaxDigits = 3;
+constexpr uint32_t kSuperBucketBits = 11;  // super-bucket = up to 2^11 buckets
+
+template <typename K>
+struct BucketDigitizer {
+    static constexpr int kDigits = kBucketMaxDigits;
+    static constexpr bool kChecks = true;
+    static constexpr bool kCheapDigit = false;
+    BucketIndexer bi;
+    uint32_t shift[kBucketMaxDigits];  // digit p = (b >> shift[p]) & 255; unused: 63 (=> 0)
+    uint32_t s_lo;                     // super-bucket = b >> s_lo
+    uint32_t used;                     // number of digit passes that can be non-trivial
+
+    static BucketDigitizer make(uint64_t n, uint64_t bound) {
+        BucketDigitizer d{};
+        d.bi = BucketIndexer::make(n, bound);
+        const uint32_t L = n > 1 ? 64 - __builtin_clzll(n - 1) : 0;  // bits of the largest bucket index
+        uint32_t db = L > kSuperBucketBits ? (L - kSuperBucketBits + 7) / 8 : 0;
+        if (db > kBucketMaxDigits) db = kBucketMaxDigits;
+        d.used = db;
+        d.s_lo = L > 8 * db ? L - 8 * db : 0;
+        for (uint32_t p = 0; p < kBucketMaxDigits; ++p) d.shift[p] = p < db ? d.s_lo + 8 * p : 63;
+        return d;
+    }
+    __device__ __forceinline__ uint32_t digit_of_bucket(uint64_t b, int pos) const {
+        return static_cast<uint32_t>(b >> shift[pos]) & (kRadix - 1);
+    }
+    __device__ __forceinline__ uint32_t digit(K key, int pos) const {
+        return digit_of_bucket(bi.bucket(static_cast<uint64_t>(key)), pos);
+    }
+    __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
+        const uint64_t b = bi.bucket(static_cast<uint64_t>(key));
+#pragma unroll
+        for (int p = 0; p < kDigits; ++p) d[p] = digit_of_bucket(b, p);
+    }
+    __device__ __forceinline__ bool in_range(K key) const { return static_cast<uint64_t>(key) <= bi.bound; }
+    __device__ __forceinline__ uint64_t super_bucket(K key) const {
+        return bi.bucket(static_cast<uint64_t>(key)) >> s_lo;
+    }
+};
+
+// -------------------------------------------------------- bucket state
+struct BucketState {
+    unsigned long long span_lo_not;  // ~(min start) of non-constant oversized super-buckets
+    unsigned long long span_hi;      // max end
+    uint32_t oversized;              // non-constant oversized super-buckets
+    uint32_t n_over;                 // oversized records written by K5
+};
+
+struct OverRec {
+    unsigned long long start;  // absolute start of the trailing oversized super-bucket
+    unsigned long long kmin, kmax;  // over the part the owner staged
+    uint32_t window;
+    uint32_t pad;
+};
+
+template <typename K>
+struct WindowSummary {  // per window: first super-bucket start, min/max of the keys before it
+    unsigned long long first;  // absolute, or ~0 if no super-bucket starts in the window
+    unsigned long long hmin, hmax;
+};
+
+// ------------------------------------------------------------------ K5
+template <int BLOCK, int IPT>
+struct WindowCfg {
+    static constexpr int kStage = BLOCK * IPT;  // keys staged per CTA
+    static constexpr int kWindow = kStage / 2;  // owned range
+    static constexpr int kCap = kStage - kWindow;  // reach past the window
+    static constexpr int kWarps = BLOCK / 32;
+};
+
+template <typename K, int BLOCK, int IPT, bool VALS>
+struct WindowSmem {
+    K keys[BLOCK * IPT];
+    uint32_t vals[VALS ? BLOCK * IPT : 1];
+    uint32_t warp_hist[BLOCK / 32][kRadix + 1];
+    uint32_t tile_start[kRadix];
+    uint32_t scan_tot[kRadix / 32];
+    unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32];
+    int first, last, end;
+};
+
+template <typename T>
+__device__ __forceinline__ T block_max_u64(T v, unsigned long long* red, int warps) {
+    unsigned long long x = warp_max<unsigned long long>(static_cast<unsigned long long>(v));
+    __syncthreads();
+    if (lane_id() == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    x = 0;
+    for (int w = 0; w < warps; ++w) x = red[w] > x ? red[w] : x;
+    return static_cast<T>(x);
+}
+
+template <typename K, typename Dz, int BLOCK, int IPT, bool VALS>
+__global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
+                                                          const RadixState* __restrict__ rst,
+                                                          BucketState* __restrict__ bst,
+                                                          WindowSummary<K>* __restrict__ summ,
+                                                          OverRec* __restrict__ over, Dz dz) {
+    using Cfg = WindowCfg<BLOCK, IPT>;
+    using Smem = WindowSmem<K, BLOCK, IPT, VALS>;
+    constexpr int kStage = Cfg::kStage, kWindow = Cfg::kWindow, kWarps = Cfg::kWarps;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    if (rst->descents == 0 || rst->first_bad != 0) return;  // sorted input / range error: nothing to do
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t lane = lane_id();
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kWindow;
+    const int avail = static_cast<int>((n - w0 < static_cast<uint64_t>(kStage) ? n - w0 : static_cast<uint64_t>(kStage)));
+    const int wlen = min(kWindow, avail);
+
+    if (tid == 0) {
+        sm.first = 0x7fffffff;
+        sm.last = -1;
+        sm.end = avail;
+    }
+    for (int j = tid; j < avail; j += BLOCK) {
+        sm.keys[j] = keys[w0 + j];
+        if (VALS) sm.vals[j] = vals[w0 + j];
+    }
+    __syncthreads();
+    // super-bucket starts in [0, wlen): first and last; first start in [wlen, avail) = end
+    int my_first = 0x7fffffff, my_last = -1, my_end = 0x7fffffff;
+    for (int j = tid; j < avail; j += BLOCK) {
+        const uint64_t p = w0 + j;
+        const bool start =
+            p == 0 || dz.super_bucket(sm.keys[j]) != dz.super_bucket(j ? sm.keys[j - 1] : keys[p - 1]);
+        if (start) {
+            if (j < wlen) {
+                my_first = min(my_first, j);
+                my_last = max(my_last, j);
+            } else {
+                my_end = min(my_end, j);
+            }
+        }
+    }
+    my_first = __reduce_min_sync(ISORT_FULL_MASK, my_first);
+    my_last = __reduce_max_sync(ISORT_FULL_MASK, my_last);
+    my_end = __reduce_min_sync(ISORT_FULL_MASK, my_end);
+    if (lane == 0) {
+        if (my_first != 0x7fffffff) atomicMin(&sm.first, my_first);
+        if (my_last >= 0) atomicMax(&sm.last, my_last);
+        if (my_end != 0x7fffffff) atomicMin(&sm.end, my_end);
+    }
+    __syncthreads();
+    const int first = sm.first < wlen ? sm.first : wlen;
+    int end = sm.end;
+
+    // summary: head = keys before the first owned super-bucket
+    {
+        K hmin = static_cast<K>(~static_cast<K>(0)), hmax = 0;
+        for (int j = tid; j < first; j += BLOCK) {
+            const K k = sm.keys[j];
+            hmin = k < hmin ? k : hmin;
+            hmax = k > hmax ? k : hmax;
+        }
+        const unsigned long long a = block_max_u64(~static_cast<unsigned long long>(hmin), sm.red_a, kWarps);
+        const unsigned long long b = block_max_u64(static_cast<unsigned long long>(hmax), sm.red_b, kWarps);
+        if (tid == 0) {
+            summ[blockIdx.x].first = first < wlen ? w0 + first : ~0ull;
+            summ[blockIdx.x].hmin = ~a;
+            summ[blockIdx.x].hmax = b;
+        }
+    }
+    if (first >= wlen) return;  // no super-bucket starts here
+
+    if (end == avail && w0 + avail < n) {
+        // The last owned super-bucket runs past the staged range: oversized.
+        // Record it (K6 resolves its end and whether it is constant); sort the rest.
+        const int ostart = sm.last;
+        K omin = static_cast<K>(~static_cast<K>(0)), omax = 0;
+        for (int j = ostart + tid; j < avail; j += BLOCK) {
+            const K k = sm.keys[j];
+            omin = k < omin ? k : omin;
+            omax = k > omax ? k : omax;
+        }
+        const unsigned long long a = block_max_u64(~static_cast<unsigned long long>(omin), sm.red_a, kWarps);
+        const unsigned long long b = block_max_u64(static_cast<unsigned long long>(omax), sm.red_b, kWarps);
+        if (tid == 0) {
+            const uint32_t r = atomicAdd(&bst->n_over, 1u);
+            over[r].start = w0 + ostart;
+            over[r].kmin = ~a;
+            over[r].kmax = b;
+            over[r].window = blockIdx.x;
+        }
+        end = ostart;
+    }
+    const int len = end - first;
+    if (len <= 1) return;
+
+    // ---- stable block radix sort of sm.keys[first, end) by (key - min)
+    K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
+    for (int j = first + tid; j < end; j += BLOCK) {
+        const K k = sm.keys[j];
+        kmin = k < kmin ? k : kmin;
+        kmax = k > kmax ? k : kmax;
+    }
+    kmin = static_cast<K>(~block_max_u64(~static_cast<unsigned long long>(kmin), sm.red_a, kWarps));
+    kmax = static_cast<K>(block_max_u64(static_cast<unsigned long long>(kmax), sm.red_b, kWarps));
+    if (kmin == kmax) return;  // one key value: arrival order is the answer
+    const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
+    const int passes = (bits + kRadixBits - 1) / kRadixBits;
+
+    K key[IPT];
+    uint32_t val[IPT];
+    const int wofs = warp * 32 * IPT + static_cast<int>(lane);
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int o = wofs + i * 32;
+        key[i] = o < len ? sm.keys[first + o] : static_cast<K>(0);
+        if (VALS) val[i] = o < len ? sm.vals[first + o] : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+    for (int pass = 0; pass < passes; ++pass) {
+        const uint32_t shift = static_cast<uint32_t>(pass * kRadixBits);
+        for (int i = tid; i < kWarps * (kRadix + 1); i += BLOCK) (&sm.warp_hist[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t rank[IPT], dg[IPT];
+        uint32_t* wh = sm.warp_hist[warp];
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int o = wofs + i * 32;
+            const uint32_t d = o < len ? static_cast<uint32_t>((static_cast<uint64_t>(key[i] - kmin) >> shift) & 255u)
+                                       : static_cast<uint32_t>(kRadix);
+            dg[i] = d;
+            const uint32_t peers = __match_any_sync(ISORT_FULL_MASK, d);
+            const int leader = 31 - __clz(peers);
+            uint32_t b = 0;
+            if (static_cast<int>(lane) == leader) {
+                b = wh[d];
+                wh[d] = b + __popc(peers);
+            }
+            b = __shfl_sync(ISORT_FULL_MASK, b, leader);
+            rank[i] = b + __popc(peers & lt);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < kRadix) {
+            uint32_t count = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = sm.warp_hist[w][tid];
+                sm.warp_hist[w][tid] = count;
+                count += c;
+            }
+            const uint32_t inc = warp_inclusive_scan(count);
+            if (lane == 31) sm.scan_tot[tid >> 5] = inc;
+            sm.tile_start[tid] = inc - count;
+        }
+        __syncthreads();
+        if (tid < kRadix) {
+            uint32_t pre = 0;
+            for (int w = 0; w < (tid >> 5); ++w) pre += sm.scan_tot[w];
+            const uint32_t start = sm.tile_start[tid] + pre;
+            for (int w = 0; w < kWarps; ++w) sm.warp_hist[w][tid] += start;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int o = wofs + i * 32;
+            if (o < len) {
+                const uint32_t p = sm.warp_hist[warp][dg[i]] + rank[i];
+                sm.keys[first + p] = key[i];
+                if (VALS) sm.vals[first + p] = val[i];
+            }
+        }
+        __syncthreads();
+        if (pass + 1 < passes) {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const int o = wofs + i * 32;
+                if (o < len) {
+                    key[i] = sm.keys[first + o];
+                    if (VALS) val[i] = sm.vals[first + o];
+                }
+            }
+        }
+    }
+    for (int j = first + tid; j < end; j += BLOCK) {
+        keys[w0 + j] = sm.keys[j];
+        if (VALS) vals[w0 + j] = sm.vals[j];
+    }
+}
+
+// ------------------------------------------------------------------ K6
+// One CTA per oversized record: walk the following windows' summaries until a
+// super-bucket start appears; combine min/max.  Non-constant => mark the span.
+template <typename K, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_resolve_oversized(const WindowSummary<K>* __restrict__ summ,
+                                                             uint32_t num_windows, const OverRec* __restrict__ over,
+                                                             BucketState* __restrict__ bst, uint64_t n) {
+    __shared__ unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32], red_c[BLOCK / 32];
+    const uint32_t nrec = bst->n_over;
+    for (uint32_t r = blockIdx.x; r < nrec; r += gridDim.x) {
+        const OverRec rec = over[r];
+        unsigned long long kmin = rec.kmin, kmax = rec.kmax;
+        unsigned long long end = n;
+        for (uint32_t base = rec.window + 1; base < num_windows; base += BLOCK) {
+            const uint32_t w = base + threadIdx.x;
+            unsigned long long f = ~0ull, hmin = ~0ull, hmax = 0;
+            if (w < num_windows) {
+                f = summ[w].first;
+                hmin = summ[w].hmin;
+                hmax = summ[w].hmax;
+            }
+            // first window (lowest index) with a start
+            unsigned long long fw = f != ~0ull ? static_cast<unsigned long long>(w) : ~0ull;
+            fw = ~block_max_u64(~fw, red_c, BLOCK / 32);
+            const bool take = w < num_windows && static_cast<unsigned long long>(w) <= fw;
+            const unsigned long long a = block_max_u64(take ? ~hmin : 0ull, red_a, BLOCK / 32);
+            const unsigned long long b = block_max_u64(take ? hmax : 0ull, red_b, BLOCK / 32);
+            kmin = (~a) < kmin ? ~a : kmin;
+            kmax = b > kmax ? b : kmax;
+            if (fw != ~0ull) {
+                end = summ[fw].first;
+                break;
+            }
+        }
+        if (threadIdx.x == 0 && kmin != kmax) {
+            atomicAdd(&bst->oversized, 1u);
+            atomicMax(&bst->span_lo_not, ~rec.start);
+            atomicMax(&bst->span_hi, end);
+        }
+        __syncthreads();
+    }
+}
+
+template <typename K>
+__global__ void k_copy_range(const K* __restrict__ src, K* __restrict__ dst, const uint32_t* __restrict__ vsrc,
+                             uint32_t* __restrict__ vdst, uint64_t count) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        dst[i] = src[i];
+        if (vdst) vdst[i] = vsrc[i];
+    }
+}
+
+}  // namespace isort

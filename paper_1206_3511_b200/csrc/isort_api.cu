@@ -1,0 +1,718 @@
+// isort_api.cu -- extern "C" boundary of libisort.so (declared in include/isort.h).
+//
+// Device entry points launch the sm_100a kernels of radix_onesweep.cuh /
+// bucket_sort.cuh on the caller's stream.  Host entry points are the drop-in
+// path behind intsort::radix_sort_lsd / bucket_sort (proj/core/src/sort.cpp):
+// H2D of the 16-byte records, pack to SoA keys + u32 position payload, device
+// sort, gather of whole records by position, D2H.  No CPU fallback exists.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/isort.h"
+#include "bucket_sort.cuh"
+#include "isort_common.cuh"
+#include "radix_onesweep.cuh"
+
+namespace isort {
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_last_error;
+thread_local uint64_t g_last_bad_index = ~0ull;
+
+int set_error(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define ISORT_CUDA_TRY(expr)                                                                     \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return ::isort::set_error(ISORT_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                      __FILE__, __LINE__);                                       \
+    } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------ observability
+// Kernel launches issued by this library (bench.py reports them as
+// gpu_launches) and an optional per-phase event trail on the launching stream
+// (bench.py turns it into the dominant kernel's live duration).
+std::atomic<uint64_t> g_launches{0};
+
+struct ProfSink {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::string> names;
+    const RadixState* st = nullptr;
+};
+thread_local ProfSink g_prof;
+
+inline void launched(int k = 1) { g_launches.fetch_add(static_cast<uint64_t>(k), std::memory_order_relaxed); }
+
+inline void prof_mark(cudaStream_t s, const char* name) {
+    if (!g_prof.on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    g_prof.ev.push_back(e);
+    g_prof.names.emplace_back(name);
+}
+
+// ----------------------------------------------------- kernel configuration
+// Tile shapes per (key width, payload).  Tile = BLOCK * IPT keys.
+template <typename K, bool VALS>
+struct PassCfg {
+    static constexpr int kBlock = 512;
+    static constexpr int kIpt = sizeof(K) == 4 ? 15 : (VALS ? 10 : 12);
+    static constexpr int kTile = kBlock * kIpt;
+};
+
+constexpr int kUpfrontBlock = 512;
+
+struct RadixLayout {
+    size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
+    uint32_t tiles = 0;
+};
+
+template <typename K>
+RadixLayout radix_layout(uint64_t n, bool vals) {
+    RadixLayout L;
+    const int tile = vals ? PassCfg<K, true>::kTile : PassCfg<K, false>::kTile;
+    L.tiles = static_cast<uint32_t>((n + tile - 1) / tile);
+    size_t off = 0;
+    L.state = off;
+    off += align_up(sizeof(RadixState));
+    L.lookback = off;
+    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * L.tiles * kRadix * sizeof(uint32_t));
+    L.keys_alt = off;
+    off += align_up(n * sizeof(K));
+    L.vals_alt = off;
+    if (vals) off += align_up(n * sizeof(uint32_t));
+    L.total = off;
+    return L;
+}
+
+// Opt a kernel into >48 KB of dynamic shared memory, once per (kernel, device).
+template <typename F>
+void set_max_smem_once(F* kernel, size_t bytes) {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
+// Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
+// bucket sort's bucket-index digits).  Buffers: kin (const) -> kout, with kalt
+// as ping-pong; the plan decides which passes run.
+template <typename K, bool VALS, typename Dz>
+int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
+                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, uint32_t* lookback,
+                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
+                          cudaStream_t s) {
+    using Cfg = PassCfg<K, VALS>;
+    constexpr int D = Dz::kDigits;
+    prof_mark(s, "start");
+    g_prof.st = st;
+    if (zero_state) {
+        const size_t bytes = reinterpret_cast<char*>(lookback) - reinterpret_cast<char*>(st) +
+                             static_cast<size_t>(D) * tiles * kRadix * sizeof(uint32_t);
+        ISORT_CUDA_TRY(cudaMemsetAsync(st, 0, bytes, s));
+        prof_mark(s, "memset");
+    }
+    const bool vec = (reinterpret_cast<uintptr_t>(kin) & 15u) == 0;
+    const uint64_t want = (n + 4ull * kUpfrontBlock - 1) / (4ull * kUpfrontBlock);
+    const unsigned grid1 = static_cast<unsigned>(want < 4ull * kNumSMs ? (want ? want : 1) : 4ull * kNumSMs);
+    if (vec)
+        k_upfront<K, Dz, kUpfrontBlock, true><<<grid1, kUpfrontBlock, 0, s>>>(kin, n, st, dz);
+    else
+        k_upfront<K, Dz, kUpfrontBlock, false><<<grid1, kUpfrontBlock, 0, s>>>(kin, n, st, dz);
+    prof_mark(s, "upfront");
+    k_plan<D><<<1, kRadix, 0, s>>>(st, n, skip_sorted ? 1 : 0);
+    prof_mark(s, "plan");
+    launched(2);
+
+    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, VALS, !Dz::kCheapDigit>;
+    auto* kern = k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS>;
+    set_max_smem_once(kern, sizeof(Smem));
+    for (int slot = 0; slot < D; ++slot) {
+        kern<<<tiles, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st,
+                                                        lookback, tiles, slot, dz);
+        static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
+                                                     "pass4", "pass5", "pass6", "pass7"};
+        prof_mark(s, kPassNames[slot]);
+    }
+    launched(D + 1);
+    const uint64_t cblocks = (n + 1023) / 1024;
+    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 8ull * kNumSMs ? cblocks : 8ull * kNumSMs), 256, 0, s>>>(
+        kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
+    prof_mark(s, "copy");
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
+template <typename K>
+int radix_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, int vmode,
+                      void* temp, size_t temp_bytes, cudaStream_t s) {
+    if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
+        return set_error(ISORT_EINVAL, "isort_radix_sort: bad vals_mode %d", vmode);
+    if (n == 0) return ISORT_OK;
+    if (n > kMaxLookbackN)
+        return set_error(ISORT_ERANGE, "isort_radix_sort: n=%llu exceeds the per-call limit %llu",
+                         (unsigned long long)n, (unsigned long long)kMaxLookbackN);
+    const bool vals = vmode != ISORT_VALS_NONE;
+    if (!kin || !kout || (vals && !vout) || (vmode == ISORT_VALS_LOAD && !vin))
+        return set_error(ISORT_EINVAL, "isort_radix_sort: null buffer");
+    const RadixLayout L = radix_layout<K>(n, vals);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_radix_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.state);
+    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
+    auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
+    RadixDigitizer<K> dz;
+    if (vals)
+        return launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, vmode == ISORT_VALS_IOTA, n, st, lb,
+                                              L.tiles, dz, true, true, s);
+    return launch_radix_pipeline<K, false>(kin, kout, kalt, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz,
+                                           true, true, s);
+}
+
+// ------------------------------------------------------- host-side helpers
+struct DeviceCtx {
+    cudaStream_t stream = nullptr;
+};
+
+std::mutex g_ctx_mu;
+DeviceCtx g_ctx[64];
+
+int use_device(int device, cudaStream_t* out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return set_error(ISORT_ECUDA, "no CUDA device available (%s); the engine has no CPU fallback",
+                         cudaGetErrorString(e));
+    if (device < 0 || device >= count || device >= 64)
+        return set_error(ISORT_EINVAL, "device %d out of range (have %d)", device, count);
+    ISORT_CUDA_TRY(cudaSetDevice(device));
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if (!g_ctx[device].stream) ISORT_CUDA_TRY(cudaStreamCreateWithFlags(&g_ctx[device].stream, cudaStreamNonBlocking));
+    *out = g_ctx[device].stream;
+    return ISORT_OK;
+}
+
+// RAII device allocation on the stream-ordered pool.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    int alloc(size_t bytes, cudaStream_t stream) {
+        s = stream;
+        ISORT_CUDA_TRY(cudaMallocAsync(&p, bytes ? bytes : 16, stream));
+        return ISORT_OK;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+__global__ void k_pack_records_u32(const isort_record* __restrict__ rec, uint32_t* __restrict__ keys, uint64_t n,
+                                   unsigned long long* __restrict__ max_key) {
+    unsigned long long m = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t k = rec[i].key;
+        keys[i] = static_cast<uint32_t>(k);
+        m = k > m ? k : m;
+    }
+    m = warp_max<unsigned long long>(m);
+    if (lane_id() == 0 && m) atomicMax(max_key, m);
+}
+
+__global__ void k_pack_records_u64(const isort_record* __restrict__ rec, uint64_t* __restrict__ keys, uint64_t n) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        keys[i] = rec[i].key;
+}
+
+__global__ void k_gather_records(const isort_record* __restrict__ in, const uint32_t* __restrict__ idx,
+                                 isort_record* __restrict__ out, uint64_t n) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = in[idx[i]];
+}
+
+inline unsigned grid_for(uint64_t n, int block = 256, int per_sm = 8) {
+    const uint64_t want = (n + block - 1) / block;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
+    return static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
+}
+
+// Sort records by key through the device: pack -> (key, position) sort -> gather.
+// `sorter(keys_in, keys_out, idx_out, n, s)` is called with u32 or u64 keys.
+template <typename Sort32, typename Sort64>
+int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t n, int device, Sort32&& sort32,
+                            Sort64&& sort64) {
+    cudaStream_t s;
+    int rc = use_device(device, &s);
+    if (rc) return rc;
+    if (n > kMaxLookbackN)
+        return set_error(ISORT_ERANGE, "n=%llu exceeds the per-call limit %llu", (unsigned long long)n,
+                         (unsigned long long)kMaxLookbackN);
+    DevBuf rec_in, rec_out, keys, keys_out, idx, maxw;
+    if ((rc = rec_in.alloc(n * sizeof(isort_record), s)) || (rc = rec_out.alloc(n * sizeof(isort_record), s)) ||
+        (rc = keys.alloc(n * sizeof(uint64_t), s)) || (rc = keys_out.alloc(n * sizeof(uint64_t), s)) ||
+        (rc = idx.alloc(n * sizeof(uint32_t), s)) || (rc = maxw.alloc(sizeof(unsigned long long), s)))
+        return rc;
+    ISORT_CUDA_TRY(cudaMemcpyAsync(rec_in.p, in, n * sizeof(isort_record), cudaMemcpyHostToDevice, s));
+    ISORT_CUDA_TRY(cudaMemsetAsync(maxw.p, 0, sizeof(unsigned long long), s));
+    k_pack_records_u32<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), keys.as<uint32_t>(), n,
+                                                  maxw.as<unsigned long long>());
+    unsigned long long mx = 0;
+    ISORT_CUDA_TRY(cudaMemcpyAsync(&mx, maxw.p, sizeof mx, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    if (mx <= 0xffffffffull) {
+        rc = sort32(keys.as<uint32_t>(), keys_out.as<uint32_t>(), idx.as<uint32_t>(), n, s);
+    } else {
+        k_pack_records_u64<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), keys.as<uint64_t>(), n);
+        rc = sort64(keys.as<uint64_t>(), keys_out.as<uint64_t>(), idx.as<uint32_t>(), n, s);
+    }
+    if (rc) {
+        cudaStreamSynchronize(s);
+        return rc;
+    }
+    k_gather_records<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), idx.as<uint32_t>(),
+                                                rec_out.as<isort_record>(), n);
+    ISORT_CUDA_TRY(cudaGetLastError());
+    ISORT_CUDA_TRY(cudaMemcpyAsync(out, rec_out.p, n * sizeof(isort_record), cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    return ISORT_OK;
+}
+
+template <typename K>
+int radix_pairs_owned(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, cudaStream_t s) {
+    const size_t tb = radix_layout<K>(n, true).total;
+    DevBuf temp;
+    int rc = temp.alloc(tb, s);
+    if (rc) return rc;
+    return radix_sort_device<K>(keys, keys_out, nullptr, idx, n, ISORT_VALS_IOTA, temp.p, tb, s);
+}
+
+__global__ void k_max_records(const isort_record* __restrict__ rec, uint64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long m = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        m = rec[i].key > m ? rec[i].key : m;
+    m = warp_max<unsigned long long>(m);
+    if (lane_id() == 0 && m) atomicMax(out, m);
+}
+
+// digit_i(key) = floor(key / divisor) mod base  (sort.cpp:87-92)
+__global__ void k_digit_keys(const isort_record* __restrict__ rec, uint64_t* __restrict__ d, uint64_t n,
+                             uint64_t divisor, uint64_t base) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        d[i] = (rec[i].key / divisor) % base;
+}
+
+__global__ void k_bucket_index(const uint64_t* __restrict__ keys, uint64_t* __restrict__ out, uint64_t m,
+                               BucketIndexer bi) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+        out[i] = keys[i] > bi.bound ? ~0ull : bi.bucket(keys[i]);
+}
+
+__global__ void k_is_sorted_u32(const uint32_t* __restrict__ keys, uint64_t n, unsigned int* __restrict__ bad) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned int b = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i + 1 < n; i += stride)
+        b |= keys[i] > keys[i + 1];
+    if (__any_sync(ISORT_FULL_MASK, b) && lane_id() == 0) atomicOr(bad, 1u);
+}
+
+
+// ------------------------------------------------------------- bucket sort
+constexpr int kWinBlock = 512;
+constexpr int kWinIpt = 16;
+
+struct BucketLayout {
+    RadixLayout r;
+    size_t bstate = 0, summ = 0, over = 0, total = 0;
+    uint32_t windows = 0;
+};
+
+template <typename K>
+BucketLayout bucket_layout(uint64_t n, bool vals) {
+    BucketLayout L;
+    L.r = radix_layout<K>(n, vals);  // state, lookback (>= 3 digit slots), alt buffers
+    L.windows = static_cast<uint32_t>((n + WindowCfg<kWinBlock, kWinIpt>::kWindow - 1) /
+                                      WindowCfg<kWinBlock, kWinIpt>::kWindow);
+    size_t off = L.r.total;
+    L.bstate = off;
+    off += align_up(sizeof(BucketState));
+    L.summ = off;
+    off += align_up(static_cast<size_t>(L.windows) * sizeof(WindowSummary<K>));
+    L.over = off;
+    off += align_up(static_cast<size_t>(L.windows) * sizeof(OverRec));
+    L.total = off;
+    return L;
+}
+
+template <typename K>
+int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
+                       int vmode, void* temp, size_t temp_bytes, cudaStream_t s) {
+    static_assert(KeyTraits<K>::kDigits >= kBucketMaxDigits, "look-back sized for the bucket digit slots");
+    g_last_bad_index = ~0ull;
+    if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
+        return set_error(ISORT_EINVAL, "isort_bucket_sort: bad vals_mode %d", vmode);
+    if (n == 0) return ISORT_OK;  // sort.cpp:139-141
+    if (n > kMaxLookbackN)
+        return set_error(ISORT_ERANGE, "isort_bucket_sort: n=%llu exceeds the per-call limit %llu",
+                         (unsigned long long)n, (unsigned long long)kMaxLookbackN);
+    const bool vals = vmode != ISORT_VALS_NONE;
+    if (!kin || !kout || (vals && !vout) || (vmode == ISORT_VALS_LOAD && !vin))
+        return set_error(ISORT_EINVAL, "isort_bucket_sort: null buffer");
+    const BucketLayout L = bucket_layout<K>(n, vals);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
+    auto* lb = reinterpret_cast<uint32_t*>(t + L.r.lookback);
+    auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
+    auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
+    auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
+    auto* summ = reinterpret_cast<WindowSummary<K>*>(t + L.summ);
+    auto* over = reinterpret_cast<OverRec*>(t + L.over);
+    const BucketDigitizer<K> dz = BucketDigitizer<K>::make(n, bound);
+    const bool iota = vmode == ISORT_VALS_IOTA;
+
+    int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, iota, n, st, lb, L.r.tiles, dz,
+                                                   true, true, s)
+                  : launch_radix_pipeline<K, false>(kin, kout, kalt, nullptr, nullptr, nullptr, false, n, st, lb,
+                                                    L.r.tiles, dz, true, true, s);
+    if (rc) return rc;
+    ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
+    if (vals) {
+        using Smem = WindowSmem<K, kWinBlock, kWinIpt, true>;
+        auto* kern = k_bucket_windows<K, BucketDigitizer<K>, kWinBlock, kWinIpt, true>;
+        set_max_smem_once(kern, sizeof(Smem));
+        kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, vout, n, st, bst, summ, over, dz);
+    } else {
+        using Smem = WindowSmem<K, kWinBlock, kWinIpt, false>;
+        auto* kern = k_bucket_windows<K, BucketDigitizer<K>, kWinBlock, kWinIpt, false>;
+        set_max_smem_once(kern, sizeof(Smem));
+        kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, nullptr, n, st, bst, summ, over, dz);
+    }
+    prof_mark(s, "windows");
+    k_resolve_oversized<K, 256><<<L.windows < 4u * kNumSMs ? L.windows : 4u * kNumSMs, 256, 0, s>>>(
+        summ, L.windows, over, bst, n);
+    prof_mark(s, "resolve");
+    launched(2);
+    ISORT_CUDA_TRY(cudaGetLastError());
+
+    // one small read-back: range error and oversized span
+    unsigned long long not_bad = 0;
+    BucketState hb{};
+    ISORT_CUDA_TRY(cudaMemcpyAsync(&not_bad, &st->first_bad, sizeof not_bad, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaMemcpyAsync(&hb, bst, sizeof hb, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    if (not_bad != 0) {
+        const uint64_t idx = ~not_bad;
+        K bad = 0;
+        ISORT_CUDA_TRY(cudaMemcpy(&bad, kin + idx, sizeof(K), cudaMemcpyDeviceToHost));
+        g_last_bad_index = idx;
+        return set_error(ISORT_EINVAL, "bucket_index: key %llu exceeds range bound %llu (sequence/spec mismatch)",
+                         (unsigned long long)bad, (unsigned long long)bound);
+    }
+    if (hb.oversized) {
+        const uint64_t lo = ~hb.span_lo_not, hi = hb.span_hi, m = hi - lo;
+        DevBuf tk, tv;
+        if ((rc = tk.alloc(m * sizeof(K), s)) || (vals && (rc = tv.alloc(m * 4, s)))) return rc;
+        RadixDigitizer<K> rdz;
+        rc = vals ? launch_radix_pipeline<K, true>(kout + lo, tk.as<K>(), kalt + lo, vout + lo, tv.as<uint32_t>(),
+                                                   valt + lo, false, m, st, lb, L.r.tiles, rdz, true, true, s)
+                  : launch_radix_pipeline<K, false>(kout + lo, tk.as<K>(), kalt + lo, nullptr, nullptr, nullptr, false,
+                                                    m, st, lb, L.r.tiles, rdz, true, true, s);
+        if (rc) return rc;
+        k_copy_range<K><<<grid_for(m), 256, 0, s>>>(tk.as<K>(), kout + lo, vals ? tv.as<uint32_t>() : nullptr,
+                                                    vals ? vout + lo : nullptr, m);
+        launched();
+        prof_mark(s, "fallback");
+        ISORT_CUDA_TRY(cudaGetLastError());
+    }
+    return ISORT_OK;
+}
+
+template <typename K>
+int bucket_pairs_owned(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, uint64_t bound, cudaStream_t s) {
+    const size_t tb = bucket_layout<K>(n, true).total;
+    DevBuf temp;
+    int rc = temp.alloc(tb, s);
+    if (rc) return rc;
+    return bucket_sort_device<K>(keys, keys_out, nullptr, idx, n, bound, ISORT_VALS_IOTA, temp.p, tb, s);
+}
+
+}  // namespace isort
+
+using namespace isort;
+
+extern "C" {
+
+const char* isort_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t isort_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int isort_profile_begin(void) {
+    for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);
+    g_prof.ev.clear();
+    g_prof.names.clear();
+    g_prof.st = nullptr;
+    g_prof.on = true;
+    return ISORT_OK;
+}
+
+int isort_profile_end(float* ms, char* names, int names_stride, int max_phases, int* count, int* n_active) {
+    g_prof.on = false;
+    const int m = static_cast<int>(g_prof.ev.size());
+    int rc = ISORT_OK;
+    if (m > 0) {
+        cudaError_t e = cudaEventSynchronize(g_prof.ev.back());
+        if (e != cudaSuccess) rc = set_error(ISORT_ECUDA, "isort_profile_end: %s", cudaGetErrorString(e));
+    }
+    int k = 0;
+    for (int i = 1; i < m && k < max_phases && rc == ISORT_OK; ++i, ++k) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, g_prof.ev[i - 1], g_prof.ev[i]);
+        if (ms) ms[k] = t;
+        if (names && names_stride > 0) {
+            std::snprintf(names + static_cast<size_t>(k) * names_stride, names_stride, "%s", g_prof.names[i].c_str());
+        }
+    }
+    if (count) *count = k;
+    if (n_active) {
+        uint32_t na = 0;
+        if (g_prof.st && rc == ISORT_OK) cudaMemcpy(&na, &g_prof.st->n_active, 4, cudaMemcpyDeviceToHost);
+        *n_active = static_cast<int>(na);
+    }
+    for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);
+    g_prof.ev.clear();
+    g_prof.names.clear();
+    return rc;
+}
+int isort_abi_version(void) { return ISORT_ABI_VERSION; }
+uint64_t isort_max_keys(void) { return kMaxLookbackN; }
+uint64_t isort_last_bad_index(void) { return g_last_bad_index; }
+
+size_t isort_radix_temp_bytes(uint64_t n, int key_bytes, int vals_mode) {
+    const bool vals = vals_mode != ISORT_VALS_NONE;
+    return key_bytes == 8 ? radix_layout<uint64_t>(n, vals).total : radix_layout<uint32_t>(n, vals).total;
+}
+
+int isort_radix_sort_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                         uint64_t n, int vals_mode, void* temp, size_t temp_bytes, void* stream) {
+    return radix_sort_device<uint32_t>(keys_in, keys_out, vals_in, vals_out, n, vals_mode, temp, temp_bytes,
+                                       static_cast<cudaStream_t>(stream));
+}
+
+int isort_radix_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                         uint64_t n, int vals_mode, void* temp, size_t temp_bytes, void* stream) {
+    return radix_sort_device<uint64_t>(keys_in, keys_out, vals_in, vals_out, n, vals_mode, temp, temp_bytes,
+                                       static_cast<cudaStream_t>(stream));
+}
+
+size_t isort_bucket_temp_bytes(uint64_t n, int key_bytes, int vals_mode) {
+    const bool vals = vals_mode != ISORT_VALS_NONE;
+    return key_bytes == 8 ? bucket_layout<uint64_t>(n, vals).total : bucket_layout<uint32_t>(n, vals).total;
+}
+
+int isort_bucket_sort_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                          uint64_t n, uint64_t range_bound, int vals_mode, void* temp, size_t temp_bytes,
+                          void* stream) {
+    return bucket_sort_device<uint32_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
+                                        temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                          uint64_t n, uint64_t range_bound, int vals_mode, void* temp, size_t temp_bytes,
+                          void* stream) {
+    return bucket_sort_device<uint64_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
+                                        temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_radix_sort_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t base, int device) {
+    g_last_bad_index = ~0ull;
+    if (base < 2) return set_error(ISORT_EINVAL, "build_radix_plan: base must be >= 2");
+    if (n == 0) return ISORT_OK;
+    if (!in || !out) return set_error(ISORT_EINVAL, "isort_radix_sort_records: null buffer");
+    return sort_records_via_device(
+        in, out, n, device,
+        [](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
+            return radix_pairs_owned<uint32_t>(k, ko, idx, m, s);
+        },
+        [](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
+            return radix_pairs_owned<uint64_t>(k, ko, idx, m, s);
+        });
+}
+
+int isort_bucket_sort_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t range_bound,
+                              int device) {
+    g_last_bad_index = ~0ull;
+    if (n == 0) return ISORT_OK;  // sort.cpp:139-141: empty input, no range check
+    if (!in || !out) return set_error(ISORT_EINVAL, "isort_bucket_sort_records: null buffer");
+    return sort_records_via_device(
+        in, out, n, device,
+        [range_bound](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
+            return bucket_pairs_owned<uint32_t>(k, ko, idx, m, range_bound, s);
+        },
+        [range_bound](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
+            return bucket_pairs_owned<uint64_t>(k, ko, idx, m, range_bound, s);
+        });
+}
+
+int isort_counting_sort_by_digit_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t base,
+                                         uint32_t digits, uint32_t digit_index, int device) {
+    if (base < 2) return set_error(ISORT_EINVAL, "counting_sort_by_digit: base must be >= 2");
+    if (digit_index >= digits)
+        return set_error(ISORT_EINVAL, "counting_sort_by_digit: digit_index %u out of range for a %u-digit plan",
+                         digit_index, digits);
+    if (n == 0) return ISORT_OK;
+    if (!in || !out) return set_error(ISORT_EINVAL, "isort_counting_sort_by_digit_records: null buffer");
+    uint64_t divisor = 1;  // pow_u64 (sort.cpp:28-34), same wrap-around arithmetic
+    for (uint32_t i = 0; i < digit_index; ++i) divisor *= base;
+    if (divisor == 0)
+        return set_error(ISORT_EINVAL, "counting_sort_by_digit: base^%u overflows 64 bits", digit_index);
+    cudaStream_t s;
+    int rc = use_device(device, &s);
+    if (rc) return rc;
+    if (n > kMaxLookbackN) return set_error(ISORT_ERANGE, "n exceeds the per-call limit");
+    // The pass is a stable sort by the digit value: compute digits on the device,
+    // then sort (digit, position) pairs and gather the records.
+    DevBuf rec_in, rec_out, dig, dig_out, idx, temp;
+    const size_t tb = radix_layout<uint64_t>(n, true).total;
+    if ((rc = rec_in.alloc(n * sizeof(isort_record), s)) || (rc = rec_out.alloc(n * sizeof(isort_record), s)) ||
+        (rc = dig.alloc(n * 8, s)) || (rc = dig_out.alloc(n * 8, s)) || (rc = idx.alloc(n * 4, s)) ||
+        (rc = temp.alloc(tb, s)))
+        return rc;
+    ISORT_CUDA_TRY(cudaMemcpyAsync(rec_in.p, in, n * sizeof(isort_record), cudaMemcpyHostToDevice, s));
+    k_digit_keys<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), dig.as<uint64_t>(), n, divisor, base);
+    rc = radix_sort_device<uint64_t>(dig.as<uint64_t>(), dig_out.as<uint64_t>(), nullptr, idx.as<uint32_t>(), n,
+                                     ISORT_VALS_IOTA, temp.p, tb, s);
+    if (rc) return rc;
+    k_gather_records<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), idx.as<uint32_t>(),
+                                                rec_out.as<isort_record>(), n);
+    ISORT_CUDA_TRY(cudaGetLastError());
+    ISORT_CUDA_TRY(cudaMemcpyAsync(out, rec_out.p, n * sizeof(isort_record), cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    return ISORT_OK;
+}
+
+int isort_build_radix_plan_records(const isort_record* in, uint64_t n, uint64_t base, uint32_t* digits, int device) {
+    if (base < 2) return set_error(ISORT_EINVAL, "build_radix_plan: base must be >= 2");
+    if (!digits) return set_error(ISORT_EINVAL, "isort_build_radix_plan_records: null output");
+    unsigned long long mx = 0;
+    if (n > 0) {
+        if (!in) return set_error(ISORT_EINVAL, "isort_build_radix_plan_records: null buffer");
+        cudaStream_t s;
+        int rc = use_device(device, &s);
+        if (rc) return rc;
+        DevBuf rec, m;
+        if ((rc = rec.alloc(n * sizeof(isort_record), s)) || (rc = m.alloc(8, s))) return rc;
+        ISORT_CUDA_TRY(cudaMemcpyAsync(rec.p, in, n * sizeof(isort_record), cudaMemcpyHostToDevice, s));
+        ISORT_CUDA_TRY(cudaMemsetAsync(m.p, 0, 8, s));
+        k_max_records<<<grid_for(n), 256, 0, s>>>(rec.as<isort_record>(), n, m.as<unsigned long long>());
+        ISORT_CUDA_TRY(cudaMemcpyAsync(&mx, m.p, 8, cudaMemcpyDeviceToHost, s));
+        ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    // minimal digits with base^digits > max (sort.cpp:67-74)
+    uint32_t d = 0;
+    uint64_t v = mx;
+    do {
+        v /= base;
+        ++d;
+    } while (v != 0);
+    *digits = d;
+    return ISORT_OK;
+}
+
+static int host_keys_u32(const uint32_t* in, uint32_t* out, uint64_t n, int device, bool bucket, uint64_t range_bound) {
+    g_last_bad_index = ~0ull;
+    if (n == 0) return ISORT_OK;
+    if (!in || !out) return set_error(ISORT_EINVAL, "null host buffer");
+    cudaStream_t s;
+    int rc = use_device(device, &s);
+    if (rc) return rc;
+    const size_t tb = bucket ? bucket_layout<uint32_t>(n, false).total : radix_layout<uint32_t>(n, false).total;
+    DevBuf din, dout, temp;
+    if ((rc = din.alloc(n * 4, s)) || (rc = dout.alloc(n * 4, s)) || (rc = temp.alloc(tb, s))) return rc;
+    ISORT_CUDA_TRY(cudaMemcpyAsync(din.p, in, n * 4, cudaMemcpyHostToDevice, s));
+    rc = bucket ? bucket_sort_device<uint32_t>(din.as<uint32_t>(), dout.as<uint32_t>(), nullptr, nullptr, n,
+                                               range_bound, ISORT_VALS_NONE, temp.p, tb, s)
+                : radix_sort_device<uint32_t>(din.as<uint32_t>(), dout.as<uint32_t>(), nullptr, nullptr, n,
+                                              ISORT_VALS_NONE, temp.p, tb, s);
+    if (rc) {
+        cudaStreamSynchronize(s);
+        return rc;
+    }
+    ISORT_CUDA_TRY(cudaMemcpyAsync(out, dout.p, n * 4, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    return ISORT_OK;
+}
+
+int isort_radix_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n, int device) {
+    return host_keys_u32(in, out, n, device, false, 0);
+}
+
+int isort_bucket_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t range_bound, int device) {
+    return host_keys_u32(in, out, n, device, true, range_bound);
+}
+
+int isort_bucket_index_u64(const uint64_t* keys, uint64_t* out, uint64_t m, uint64_t bucket_count,
+                           uint64_t range_bound, void* stream) {
+    if (bucket_count == 0) return set_error(ISORT_EINVAL, "bucket_index: bucket_count must be >= 1");
+    if (m == 0) return ISORT_OK;
+    if (!keys || !out) return set_error(ISORT_EINVAL, "isort_bucket_index_u64: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    k_bucket_index<<<grid_for(m), 256, 0, s>>>(keys, out, m, BucketIndexer::make(bucket_count, range_bound));
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
+int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* stream) {
+    if (!result) return set_error(ISORT_EINVAL, "isort_is_sorted_u32: null result");
+    if (n < 2) {
+        *result = 1;
+        return ISORT_OK;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevBuf flag;
+    int rc = flag.alloc(4, s);
+    if (rc) return rc;
+    ISORT_CUDA_TRY(cudaMemsetAsync(flag.p, 0, 4, s));
+    k_is_sorted_u32<<<grid_for(n), 256, 0, s>>>(keys, n, flag.as<unsigned int>());
+    unsigned int bad = 0;
+    ISORT_CUDA_TRY(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    *result = bad ? 0 : 1;
+    return ISORT_OK;
+}
+
+}  // extern "C"

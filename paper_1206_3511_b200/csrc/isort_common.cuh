@@ -1,0 +1,98 @@
+// isort_common.cuh -- shared device helpers for the B200 integer-sort engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ISORT_FULL_MASK 0xffffffffu
+
+namespace isort {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;  // bins per digit pass
+constexpr int kMaxDigits = 8;            // u64 keys: 8 x 8-bit digits
+constexpr int kNumSMs = 148;             // B200; grids are sized in multiples of this
+
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<uint32_t> {
+    static constexpr int kDigits = 4;
+};
+template <>
+struct KeyTraits<uint64_t> {
+    static constexpr int kDigits = 8;
+};
+
+// ---------------------------------------------------------------- memory ops
+// Decoupled look-back status words live in L2; relaxed gpu-scope atomics are
+// sufficient because the flag and the count share one 32-bit word.
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Streaming read-only load (input keys are read exactly once per pass).
+__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint64_t ldg_stream(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ldg_stream_v4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K key, uint32_t shift) {
+    return static_cast<uint32_t>(key >> shift) & (kRadix - 1);
+}
+
+// Inclusive warp scan (Kogge-Stone over shuffles).
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(ISORT_FULL_MASK, v, o);
+        if (lane_id() >= static_cast<uint32_t>(o)) v += t;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const T t = __shfl_xor_sync(ISORT_FULL_MASK, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(ISORT_FULL_MASK, v, o);
+    return v;
+}
+
+}  // namespace isort

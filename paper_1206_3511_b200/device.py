@@ -1,0 +1,109 @@
+"""Device-resident sorts over torch tensors (torch is plumbing: memory + streams).
+
+Keys are u32 or u64 bit patterns held in ``torch.int32`` / ``torch.int64``
+(or ``torch.uint32`` / ``torch.uint64``) CUDA tensors; payloads are 32-bit.
+Each call goes straight to the C ABI (include/isort.h) on the current torch
+stream.  :class:`Sorter` keeps its output and temp buffers so repeated calls
+(benchmarks) allocate nothing.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_U32 = {torch.int32, getattr(torch, "uint32", torch.int32)}
+_U64 = {torch.int64, getattr(torch, "uint64", torch.int64)}
+
+RADIX = "radix"
+BUCKET = "bucket"
+
+
+def _key_bytes(t: torch.Tensor) -> int:
+    if t.dtype in _U32:
+        return 4
+    if t.dtype in _U64:
+        return 8
+    raise TypeError(f"keys must be 32- or 64-bit integer tensors, got {t.dtype}")
+
+
+def _check_cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise _lib.CudaError(_lib.ISORT_ECUDA, f"{what} must be a CUDA tensor (the engine has no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+
+
+class Sorter:
+    """Reusable device sort of n keys (+ optional u32 payload).
+
+    ``vals``: None (keys only), "iota" (payload = original position, generated on
+    the device) or "load" (a payload tensor is passed to :meth:`__call__`).
+    """
+
+    def __init__(self, n: int, key_bytes: int = 4, algorithm: str = RADIX, vals: str | None = None,
+                 range_bound: int | None = None, device: torch.device | str = "cuda"):
+        if algorithm not in (RADIX, BUCKET):
+            raise ValueError(f"unknown algorithm {algorithm!r}")
+        if algorithm == BUCKET and range_bound is None:
+            range_bound = (1 << (8 * key_bytes)) - 1
+        self.n, self.key_bytes, self.algorithm, self.range_bound = n, key_bytes, algorithm, range_bound
+        self.vmode = {None: _lib.VALS_NONE, "load": _lib.VALS_LOAD, "iota": _lib.VALS_IOTA}[vals]
+        lib = _lib.load()
+        tb = (lib.isort_radix_temp_bytes if algorithm == RADIX else lib.isort_bucket_temp_bytes)(
+            n, key_bytes, self.vmode)
+        dt = torch.int32 if key_bytes == 4 else torch.int64
+        self.device = torch.device(device)
+        self.keys_out = torch.empty(max(n, 1), dtype=dt, device=self.device)[:n]
+        self.vals_out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)[:n] if vals else None
+        self.temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
+        self.temp_bytes = tb
+
+    def __call__(self, keys: torch.Tensor, vals_in: torch.Tensor | None = None, stream=None):
+        _check_cuda(keys, "keys")
+        if keys.numel() != self.n or _key_bytes(keys) != self.key_bytes:
+            raise ValueError("keys do not match the Sorter's shape/width")
+        if self.vmode == _lib.VALS_LOAD:
+            if vals_in is None or vals_in.numel() != self.n:
+                raise ValueError("vals='load' needs a payload tensor of n elements")
+            _check_cuda(vals_in, "vals")
+        lib = _lib.load()
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        vin = vals_in.data_ptr() if (vals_in is not None and self.vmode == _lib.VALS_LOAD) else None
+        vout = self.vals_out.data_ptr() if self.vals_out is not None else None
+        if self.algorithm == RADIX:
+            fn = lib.isort_radix_sort_u32 if self.key_bytes == 4 else lib.isort_radix_sort_u64
+            rc = fn(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n, self.vmode,
+                    self.temp.data_ptr(), self.temp_bytes, s)
+        else:
+            fn = lib.isort_bucket_sort_u32 if self.key_bytes == 4 else lib.isort_bucket_sort_u64
+            rc = fn(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n, int(self.range_bound),
+                    self.vmode, self.temp.data_ptr(), self.temp_bytes, s)
+        _lib.check(rc)
+        return self.keys_out, self.vals_out
+
+
+def radix_sort(keys: torch.Tensor, vals: torch.Tensor | None = None, iota: bool = False):
+    """One-shot device LSD radix sort.  Returns (sorted keys, payload or None)."""
+    mode = "load" if vals is not None else ("iota" if iota else None)
+    s = Sorter(keys.numel(), _key_bytes(keys), RADIX, mode, device=keys.device)
+    k, v = s(keys, vals)
+    return k, v
+
+
+def bucket_sort(keys: torch.Tensor, range_bound: int, vals: torch.Tensor | None = None, iota: bool = False):
+    """One-shot device bucket sort over [0, range_bound]."""
+    mode = "load" if vals is not None else ("iota" if iota else None)
+    s = Sorter(keys.numel(), _key_bytes(keys), BUCKET, mode, range_bound=range_bound, device=keys.device)
+    k, v = s(keys, vals)
+    return k, v
+
+
+def is_sorted_u32(keys: torch.Tensor) -> bool:
+    import ctypes
+
+    _check_cuda(keys, "keys")
+    r = ctypes.c_int(0)
+    _lib.check(_lib.load().isort_is_sorted_u32(keys.data_ptr(), keys.numel(), ctypes.byref(r),
+                                               torch.cuda.current_stream(keys.device).cuda_stream))
+    return bool(r.value)

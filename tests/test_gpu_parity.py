@@ -1,0 +1,248 @@
+"""GPU parity: the sm_100a engine against the oracle and the reference's golden
+vectors.  Bit-exact for keys and payload (positions) -- a stable sort has one
+correct output.  Run with ``-m gpu`` on a B200."""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1206_3511_b200 as isort
+from oracle.binding import RECORD_DTYPE
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+U32_MAX = (1 << 32) - 1
+TILE = 7680  # u32 keys-only / pairs one-sweep tile
+
+
+def recs(keys):
+    a = np.empty(len(keys), dtype=RECORD_DTYPE)
+    a["key"] = np.asarray(keys, dtype=np.uint64)
+    a["tag"] = np.arange(len(keys), dtype=np.uint64)
+    return a
+
+
+def dev_sort(keys_np: np.ndarray, algorithm="radix", payload="iota", range_bound=None):
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    kb = keys_np.dtype.itemsize
+    t = torch.from_numpy(keys_np.view(np.int32 if kb == 4 else np.int64).copy()).cuda()
+    s = device.Sorter(keys_np.size, kb, algorithm, payload, range_bound=range_bound)
+    k, v = s(t)
+    torch.cuda.synchronize()
+    ko = k.cpu().numpy().view(keys_np.dtype)
+    vo = v.cpu().numpy().view(np.uint32) if v is not None else None
+    return ko, vo
+
+
+# ------------------------------------------------------- golden vectors (records API)
+@pytest.fixture(scope="module")
+def golden():
+    z = np.load(os.path.join(GOLDEN, "reference_vectors.npz"))
+    with open(os.path.join(GOLDEN, "reference_vectors.json")) as f:
+        meta = json.load(f)
+    return z, meta
+
+
+def test_records_radix_matches_reference_vectors(cuda, golden):
+    z, meta = golden
+    for i, sp in enumerate(meta):
+        s = recs(z[f"in_{i}"])
+        out10 = isort.radix_sort_lsd(s, 10)
+        assert np.array_equal(out10["tag"], z[f"radix10_{i}"]), sp
+        assert np.array_equal(out10["key"], s["key"][z[f"radix10_{i}"]]), sp
+        assert np.array_equal(isort.radix_sort_lsd(s, 256)["tag"], z[f"radix256_{i}"]), sp
+
+
+def test_records_bucket_matches_reference_vectors(cuda, golden):
+    z, meta = golden
+    for i, sp in enumerate(meta):
+        s = recs(z[f"in_{i}"])
+        out = isort.bucket_sort(s, sp["bound"])
+        assert np.array_equal(out["tag"], z[f"bucket_{i}"]), sp
+
+
+def test_records_plan_and_counting_pass_match_reference(cuda, golden):
+    z, meta = golden
+    for i, sp in enumerate(meta):
+        s = recs(z[f"in_{i}"])
+        assert isort.build_radix_plan(s, 10).digits == sp["digits10"]
+        assert isort.build_radix_plan(s, 256).digits == sp["digits256"]
+        if sp["n"]:
+            d = sp["digits10"]
+            out = isort.counting_sort_by_digit(s, isort.RadixPlan(10, d), d - 1)
+            assert np.array_equal(out["tag"], z[f"count_top_{i}"]), sp
+
+
+def test_device_bucket_index_matches_reference(cuda, golden):
+    z, _ = golden
+    bi = z["bucket_index"]
+    # group by (count, bound) is unnecessary: one call per sample keeps the test simple
+    for key, count, bound, want in bi[:300].tolist():
+        assert isort.bucket_index(int(key), int(count), int(bound)) == int(want)
+    with pytest.raises(isort.InvalidArgument, match="exceeds range bound"):
+        isort.bucket_index(1000, 10, 999)
+    with pytest.raises(isort.InvalidArgument):
+        isort.bucket_index(0, 0, 999)
+
+
+# ------------------------------------------------------- device API vs oracle
+SIZES = [1, 2, 31, 32, 33, 1000, TILE - 1, TILE, TILE + 1, 2 * TILE + 17, 100_000, 1_000_003]
+
+
+def _dist(name, n, rng):
+    if name == "uniform":
+        return rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    if name == "small_range":
+        return rng.integers(0, 1024, size=n, dtype=np.uint64).astype(np.uint32)
+    if name == "all_equal":
+        return np.full(n, 123456789, dtype=np.uint32)
+    if name == "sorted":
+        return np.sort(rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32))
+    if name == "reverse":
+        return np.sort(rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32))[::-1].copy()
+    if name == "one_digit":  # only digit 2 varies
+        return (rng.integers(0, 256, size=n, dtype=np.uint64).astype(np.uint32) << 16) | 0x0A0000BB
+    if name == "max_key":
+        a = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        a[:: max(1, n // 7)] = U32_MAX
+        return a
+    if name == "two_values":
+        return np.where(rng.integers(0, 2, size=n) > 0, U32_MAX, 0).astype(np.uint32)
+    raise KeyError(name)
+
+
+DISTS = ["uniform", "small_range", "all_equal", "sorted", "reverse", "one_digit", "max_key", "two_values"]
+
+
+@pytest.mark.parametrize("algorithm", ["radix", "bucket"])
+@pytest.mark.parametrize("dist", DISTS)
+def test_device_u32_pairs_bit_exact(cuda, oracle, algorithm, dist):
+    rng = np.random.default_rng(hash((algorithm, dist)) & 0xFFFF)
+    for n in SIZES:
+        k = _dist(dist, n, rng)
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        got_k, got_i = dev_sort(k, algorithm, "iota", range_bound=U32_MAX)
+        assert np.array_equal(got_k, want_k), (algorithm, dist, n)
+        assert np.array_equal(got_i, want_i), (algorithm, dist, n)
+
+
+@pytest.mark.parametrize("algorithm", ["radix", "bucket"])
+def test_device_u32_keys_only(cuda, oracle, algorithm):
+    rng = np.random.default_rng(5)
+    for dist in DISTS:
+        for n in (0, 1, 5000, TILE * 3 + 1, 2_000_000):
+            k = _dist(dist, n, rng) if n else np.zeros(0, dtype=np.uint32)
+            got, _ = dev_sort(k, algorithm, None, range_bound=U32_MAX)
+            assert np.array_equal(got, np.sort(k)), (algorithm, dist, n)
+
+
+def test_device_u32_loaded_payload(cuda, oracle):
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(11)
+    n = 300_001
+    k = rng.integers(0, 1 << 20, size=n, dtype=np.uint64).astype(np.uint32)
+    v = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    order = np.argsort(k, kind="stable")
+    for alg in ("radix", "bucket"):
+        s = device.Sorter(n, 4, alg, "load", range_bound=(1 << 20) - 1)
+        ko, vo = s(torch.from_numpy(k.view(np.int32)).cuda(), torch.from_numpy(v.view(np.int32)).cuda())
+        assert np.array_equal(ko.cpu().numpy().view(np.uint32), k[order])
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), v[order])
+
+
+@pytest.mark.parametrize("algorithm", ["radix", "bucket"])
+def test_device_u64_pairs(cuda, algorithm):
+    rng = np.random.default_rng(17)
+    for n, hi in [(1, 40), (9999, 40), (200_001, 40), (200_001, 64), (50_000, 8)]:
+        k = rng.integers(0, 1 << min(hi, 63), size=n, dtype=np.uint64)
+        if hi == 64:
+            k |= rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(63)
+        want = np.argsort(k, kind="stable").astype(np.uint32)
+        got_k, got_i = dev_sort(k, algorithm, "iota", range_bound=(1 << 64) - 1)
+        assert np.array_equal(got_i, want), (algorithm, n, hi)
+        assert np.array_equal(got_k, k[want])
+
+
+# ------------------------------------------------------- bucket-specific semantics
+@pytest.mark.parametrize("bound", [U32_MAX, 1023, 1 << 40, 10**8, 999_999, (1 << 64) - 1, 3 * 10**9 + 7])
+def test_bucket_range_bounds(cuda, oracle, bound):
+    rng = np.random.default_rng(bound & 0xFFFF)
+    hi = min(bound, U32_MAX)
+    for n in (10, 4097, 123_457):
+        k = rng.integers(0, hi + 1, size=n, dtype=np.uint64).astype(np.uint32)
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        got_k, got_i = dev_sort(k, "bucket", "iota", range_bound=bound)
+        assert np.array_equal(got_i, want_i), (bound, n)
+
+
+def test_bucket_range_error_names_first_offending_key(cuda):
+    s = recs([5, 3, 11, 2, 12])
+    with pytest.raises(isort.InvalidArgument, match=r"bucket_index: key 11 exceeds range bound 10 "
+                                                    r"\(sequence/spec mismatch\)"):
+        isort.bucket_sort(s, 10)
+    from paper_1206_3511_b200 import _lib
+
+    assert _lib.load().isort_last_bad_index() == 2
+    with pytest.raises(isort.InvalidArgument):
+        isort.bucket_sort(recs([11]), 10)  # test_sort.cpp:192
+
+
+def test_bucket_oversized_super_buckets(cuda, oracle):
+    """All keys in one bucket (M far above the keys): one oversized, non-constant
+    super-bucket -> radix fallback; and constant oversized super-buckets (heavy
+    duplicates, config 3 shape) that must keep arrival order."""
+    rng = np.random.default_rng(3)
+    n = 1_000_000
+    small = rng.integers(0, 1024, size=n, dtype=np.uint64).astype(np.uint32)
+    for bound in (U32_MAX, 1023):
+        want_k, want_i = oracle.sort_u32(small, with_index=True)
+        got_k, got_i = dev_sort(small, "bucket", "iota", range_bound=bound)
+        assert np.array_equal(got_i, want_i), bound
+    mix = oracle.mixture_u32(2_000_000, 42)
+    want_k, want_i = oracle.sort_u32(mix, with_index=True)
+    got_k, got_i = dev_sort(mix, "bucket", "iota", range_bound=U32_MAX)
+    assert np.array_equal(got_i, want_i)
+
+
+# ------------------------------------------------------- config-shaped checksums (10^6)
+def test_config_shaped_checksums_match_reference(cuda, oracle):
+    with open(os.path.join(GOLDEN, "reference_checksums.json")) as f:
+        checks = json.load(f)
+    n = 1_000_000
+    inputs = {
+        "u32_uniform": oracle.generate(1, n, U32_MAX, 42),
+        "u32_small_range_1023": oracle.generate(1, n, 1023, 42),
+        "u32_sorted": oracle.generate(2, n, U32_MAX, 42),
+    }
+    rev = inputs["u32_sorted"][::-1].copy()
+    rev["tag"] = np.arange(n, dtype=np.uint64)
+    inputs["u32_reverse"] = rev
+    inputs["u32_mixture"] = recs(oracle.mixture_u32(n, 42))
+    for name, seq in inputs.items():
+        c = checks[name]
+        assert hashlib.sha256(seq["key"].astype(np.uint32).tobytes()).hexdigest() == c["input_sha256"], name
+        for out in (isort.radix_sort_lsd(seq, 256), isort.radix_sort_lsd(seq, 10), isort.bucket_sort(seq, U32_MAX)):
+            assert hashlib.sha256(out.tobytes()).hexdigest() == c["sorted_records_sha256"], name
+
+
+# ------------------------------------------------------- BASELINE-size properties (10^8)
+def test_full_size_radix_and_bucket_10e8(cuda, oracle):
+    n = 100_000_000
+    k = oracle.uniform_u32(n, 42)
+    want_k, want_i = oracle.sort_u32(k, with_index=True)
+    for alg in ("radix", "bucket"):
+        got_k, got_i = dev_sort(k, alg, "iota", range_bound=U32_MAX)
+        assert np.array_equal(got_k, want_k), alg
+        assert np.array_equal(got_i, want_i), alg
+        got_k, _ = dev_sort(k, alg, None, range_bound=U32_MAX)
+        assert np.array_equal(got_k, want_k), alg
