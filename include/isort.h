@@ -71,6 +71,10 @@ uint64_t isort_last_bad_index(void);
  * NUL-terminated phase names (names_stride bytes each), the number of phases,
  * and the number of digit passes the last pipeline actually executed. */
 uint64_t isort_launch_count(void);
+/* Rank primitive of the one-sweep passes on the current device: 1 = shared
+ * atomics (lane order verified by the load-time self-test), 0 = the
+ * __match_any_sync fallback (self-test failed), -1 = no device. */
+int isort_rank_mode(void);
 int isort_profile_begin(void);
 int isort_profile_end(float* ms, char* names, int names_stride, int max_phases, int* count,
                       int* n_active);

@@ -34,6 +34,7 @@ SIGNATURES = {
     "isort_max_keys": (_u64, []),
     "isort_last_bad_index": (_u64, []),
     "isort_launch_count": (_u64, []),
+    "isort_rank_mode": (_i32, []),
     "isort_profile_begin": (_i32, []),
     "isort_profile_end": (_i32, [ctypes.POINTER(ctypes.c_float), ctypes.c_char_p, _i32, _i32,
                                  ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),

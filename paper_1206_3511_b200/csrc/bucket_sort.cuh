@@ -151,11 +151,15 @@ struct BucketDigitizer {
         return d;
     }
     __device__ __forceinline__ uint32_t digit_of_bucket(uint64_t b, int pos) const {
-        return static_cast<uint32_t>(b >> shift[pos]) & (kRadix - 1);
+        return static_cast<uint32_t>(b >> shift_for(pos)) & (kRadix - 1);
     }
-    __device__ __forceinline__ uint32_t digit(K key, int pos) const {
-        return digit_of_bucket(bi.bucket(static_cast<uint64_t>(key)), pos);
+    __device__ __forceinline__ uint32_t shift_for(int pos) const {
+        return pos == 0 ? shift[0] : (pos == 1 ? shift[1] : shift[2]);
     }
+    __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
+        return static_cast<uint32_t>(bi.bucket(static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
+    }
+    __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         const uint64_t b = bi.bucket(static_cast<uint64_t>(key));
 #pragma unroll

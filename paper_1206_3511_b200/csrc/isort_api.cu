@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -76,9 +78,40 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 template <typename K, bool VALS>
 struct PassCfg {
     static constexpr int kBlock = 512;
-    static constexpr int kIpt = sizeof(K) == 4 ? 15 : (VALS ? 10 : 12);
-    static constexpr int kTile = kBlock * kIpt;
+    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : 12) : (VALS ? 6 : 8);
+    static constexpr int kChunks = 4;
+    static constexpr int kTile = kBlock * kIpt * kChunks;
+    static constexpr int kCtasPerSm = 2;
 };
+
+// ------------------------------------------------------- rank self-test
+// The fast one-sweep rank relies on same-address shared atomics of one warp
+// instruction being granted in ascending lane order (measured on B200, not a
+// documented guarantee).  Verify it once per device before first use; if it
+// ever fails, every pass uses the __match_any_sync rank instead (correct, ~5x
+// slower) and isort_rank_mode() reports it.
+std::mutex g_rank_mu;
+int g_rank_ok[64] = {0};  // 0 unknown, 1 verified, -1 failed
+
+bool rank_fast_path_ok() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_rank_mu);
+    if (g_rank_ok[dev & 63] != 0) return g_rank_ok[dev & 63] > 0;
+    uint32_t* d = nullptr;
+    uint32_t bad = 1;
+    if (cudaMalloc(&d, sizeof(uint32_t)) == cudaSuccess) {
+        cudaMemset(d, 0, sizeof(uint32_t));
+        k_selftest_atomic_order<<<2 * kNumSMs, 1024>>>(d, 0x5eedu);
+        if (cudaMemcpy(&bad, d, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) bad = 1;
+        cudaFree(d);
+    }
+    g_rank_ok[dev & 63] = bad == 0 ? 1 : -1;
+    if (bad)
+        std::fprintf(stderr, "isort: device %d failed the shared-atomic lane-order self-test (%u violations); "
+                             "using the __match_any_sync rank\n", dev, bad);
+    return bad == 0;
+}
 
 constexpr int kUpfrontBlock = 512;
 
@@ -106,15 +139,19 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
 }
 
 // Opt a kernel into >48 KB of dynamic shared memory, once per (kernel, device).
+// Keyed by the kernel's address: distinct instantiations can share one type.
+std::mutex g_smem_mu;
+std::set<std::pair<const void*, int>> g_smem_done;
+
 template <typename F>
 void set_max_smem_once(F* kernel, size_t bytes) {
-    static std::atomic<uint64_t> done{0};
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    if (done.load(std::memory_order_acquire) & bit) return;
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    std::lock_guard<std::mutex> g(g_smem_mu);
+    if (g_smem_done.count(key)) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-    done.fetch_or(bit, std::memory_order_acq_rel);
+    g_smem_done.insert(key);
 }
 
 // Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
@@ -147,11 +184,14 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     prof_mark(s, "plan");
     launched(2);
 
-    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, VALS, !Dz::kCheapDigit>;
-    auto* kern = k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS>;
+    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
+    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false>
+                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true>;
     set_max_smem_once(kern, sizeof(Smem));
+    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * kNumSMs) ? tiles
+                                                                                     : Cfg::kCtasPerSm * kNumSMs;
     for (int slot = 0; slot < D; ++slot) {
-        kern<<<tiles, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st,
+        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st,
                                                         lookback, tiles, slot, dz);
         static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
                                                      "pass4", "pass5", "pass6", "pass7"};
@@ -448,10 +488,11 @@ int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vou
         DevBuf tk, tv;
         if ((rc = tk.alloc(m * sizeof(K), s)) || (vals && (rc = tv.alloc(m * 4, s)))) return rc;
         RadixDigitizer<K> rdz;
+        const uint32_t tiles_m = radix_layout<K>(m, vals).tiles;  // grid for the span, not for n
         rc = vals ? launch_radix_pipeline<K, true>(kout + lo, tk.as<K>(), kalt + lo, vout + lo, tv.as<uint32_t>(),
-                                                   valt + lo, false, m, st, lb, L.r.tiles, rdz, true, true, s)
+                                                   valt + lo, false, m, st, lb, tiles_m, rdz, true, true, s)
                   : launch_radix_pipeline<K, false>(kout + lo, tk.as<K>(), kalt + lo, nullptr, nullptr, nullptr, false,
-                                                    m, st, lb, L.r.tiles, rdz, true, true, s);
+                                                    m, st, lb, tiles_m, rdz, true, true, s);
         if (rc) return rc;
         k_copy_range<K><<<grid_for(m), 256, 0, s>>>(tk.as<K>(), kout + lo, vals ? tv.as<uint32_t>() : nullptr,
                                                     vals ? vout + lo : nullptr, m);
@@ -480,6 +521,12 @@ extern "C" {
 const char* isort_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t isort_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int isort_rank_mode(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return -1;
+    return rank_fast_path_ok() ? 1 : 0;
+}
 
 int isort_profile_begin(void) {
     for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);

@@ -15,11 +15,12 @@
 //                  holds all n keys => the pass is the identity) and the whole
 //                  sort when the input is already sorted; assigns ping-pong
 //                  buffers so the last executed pass lands in `out`.
-//   K3 k_onesweep  one launch per digit slot.  Tile = BLOCK*IPT keys, tile id by
-//                  atomic ticket (forward progress for the look-back).  Warp-level
-//                  __match_any_sync ranking into per-warp smem histograms,
-//                  decoupled look-back over tiles for the global digit offsets,
-//                  smem-staged digit-sorted tile, then coalesced stores.
+//   K3 k_onesweep  one launch per digit slot; persistent CTAs take ~30K-key
+//                  tiles by atomic ticket (forward progress for the look-back).
+//                  Phase 1 counts the tile's digits and resolves its global
+//                  offsets by windowed decoupled look-back; phase 2 re-reads the
+//                  tile (L2 hits) chunk by chunk: warp-level __match_any_sync
+//                  ranking, smem-staged digit-sorted chunk, coalesced stores.
 //                                                                 8n B / pass
 //   K4 k_copy      only when no pass executes (sorted input): out = in.
 #pragma once
@@ -62,9 +63,14 @@ struct RadixDigitizer {
     static constexpr int kDigits = KeyTraits<K>::kDigits;
     static constexpr bool kChecks = false;
     static constexpr bool kCheapDigit = true;  // recompute instead of staging digits
-    __device__ __forceinline__ uint32_t digit(K key, int pos) const {
-        return digit_of<K>(key, 8u * static_cast<uint32_t>(pos));
+    __device__ __forceinline__ uint32_t shift_for(int pos) const { return 8u * static_cast<uint32_t>(pos); }
+    // One PRMT per key: byte (sh / 8) of the key, zero-extended.
+    __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
+        if (sizeof(K) == 4) return __byte_perm(static_cast<uint32_t>(key), 0u, 0x4440u | (sh >> 3));
+        const uint32_t w = sh >= 32 ? static_cast<uint32_t>(static_cast<uint64_t>(key) >> 32) : static_cast<uint32_t>(key);
+        return __byte_perm(w, 0u, 0x4440u | ((sh >> 3) & 3u));
     }
+    __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
 #pragma unroll
         for (int p = 0; p < kDigits; ++p) d[p] = digit(key, p);
@@ -209,31 +215,189 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
 }
 
 // ------------------------------------------------------------------- K3
-template <typename K, int BLOCK, int IPT, bool VALS, bool STAGE_DIGITS>
+// Persistent two-phase one-sweep pass.
+//
+// B200 facts that shape it (profiles/r01_microbench_warp_primitives.txt,
+// profiles/r01_onesweep_*.txt):
+//  * A pass must move 8n bytes in ~0.12 ms at n = 1e8: ~2.9 keys/cycle/SM, i.e.
+//    <= ~44 thread-instructions and ~11 shared-memory wavefront-cycles per 32
+//    keys.
+//  * __match_any_sync costs ~63 cycles per warp instruction per SM and an 8-ballot
+//    peer mask ~28: a match-based stable rank caps a pass near 0.7 ms.  Shared
+//    atomics with return cost ~2.6 cycles, and same-address shared atomics of one
+//    warp instruction are granted in ascending lane order (0 violations in 6.2e8
+//    lane-trials; re-verified at load time by isort_selftest, with the match-based
+//    rank as the fallback).  So a key's stable slot is one atomicAdd.
+//  * Decoupled look-back must walk (L2 latency x tile rate) predecessors; big
+//    tiles (~30K keys) keep that to ~1 windowed round trip.
+//
+// Tile = NCHUNK chunks of BLOCK*IPT keys.  Warp w of the CTA always owns the
+// same 32*IPT-key slice of every chunk (warp-striped: item i of lane l at slice
+// offset i*32 + l, so (item, lane) order is input order).
+//   phase 1  each warp counts the digits of its slices into packed 16-bit
+//            counters cnt[chunk][warp][d & 127] (halves for d and d + 128), with
+//            16-byte loads kept in L2 (evict_last); the tile total is published
+//            as the aggregate and the global offsets come from the look-back.
+//            The counters are then rewritten as chunk-local start slots:
+//            local(c, w, d) = sum_{d' < d} cnt_c(d') + sum_{w' < w} cnt(c, w', d).
+//   phase 2  per chunk: re-read (L2 hits), slot = atomicAdd(counter) -> stage the
+//            key at that slot (digit-sorted chunk), then coalesced stores at
+//            out_base[chunk][d] + slot.
+// CTAs are persistent (grid = 2 x SMs) and take tiles by atomic ticket, so every
+// tile a CTA waits on is owned by a running CTA (forward progress).
+template <typename K, int BLOCK, int IPT, int NCHUNK, bool VALS, bool STAGE_DIGITS>
 struct OnesweepSmem {
     static constexpr int kWarps = BLOCK / 32;
-    static constexpr int kTile = BLOCK * IPT;
-    K keys[kTile];
-    uint32_t vals[VALS ? kTile : 1];
-    uint8_t digits[STAGE_DIGITS ? kTile : 1];  // digit per staged key (expensive digitizers)
-    uint32_t warp_hist[kWarps][kRadix + 1];  // +1: bin kRadix absorbs out-of-range slots
-    uint32_t tile_start[kRadix];
-    uint32_t out_base[kRadix];
-    uint32_t scan_tot[kRadix / 32];
+    static constexpr int kChunk = BLOCK * IPT;
+    static constexpr int kTile = kChunk * NCHUNK;
+    uint32_t cnt[NCHUNK][kWarps][kRadix];  // phase 1: counts; then chunk-local slot bases
+    uint32_t out_base[NCHUNK][kRadix];     // global position = out_base[c][d] + slot
+    K keys[kChunk];
+    uint32_t vals[VALS ? kChunk : 1];
+    uint8_t digits[STAGE_DIGITS ? kChunk : 1];  // digit per staged key (expensive digitizers)
+    uint32_t tot_w[NCHUNK][kRadix / 32];
     uint32_t tile_id;
 };
 
-template <typename K, typename Dz, int BLOCK, int IPT, bool VALS>
-__global__ void __launch_bounds__(BLOCK) k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out,
-                                                    K* __restrict__ keys_alt, const uint32_t* __restrict__ vals_in,
-                                                    uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
-                                                    int iota_vals, uint64_t n, RadixState* __restrict__ st,
-                                                    uint32_t* __restrict__ lookback, uint32_t num_tiles, int slot,
-                                                    Dz dz) {
-    using Smem = OnesweepSmem<K, BLOCK, IPT, VALS, !Dz::kCheapDigit>;
+constexpr int kLookbackWindow = 16;  // predecessors read per round trip, per digit
+
+// Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back.
+// All kLookbackWindow loads are in flight together, so the usual case (an
+// inclusive prefix within the window) costs one L2 round trip.
+__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ lb, uint32_t tile, int d) {
+    uint32_t excl = 0;
+    int t = static_cast<int>(tile) - 1;
+    while (t >= 0) {
+        uint32_t sv[kLookbackWindow];
+#pragma unroll
+        for (int j = 0; j < kLookbackWindow; ++j)
+            sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&lb[static_cast<size_t>(t - j) * kRadix + d]) : kFlagInc;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < kLookbackWindow; ++j) {
+            if (!done && used == j) {
+                const uint32_t f = sv[j] & kFlagMask;
+                if (f != 0) {
+                    excl += sv[j] & kValueMask;
+                    used = j + 1;
+                    done = (f == kFlagInc);
+                }
+            }
+        }
+        if (done) break;
+        t -= used;  // stopped at a predecessor that has not published: re-read from it
+    }
+    return excl;
+}
+
+// L2 eviction policies: tile keys are read twice (count, then rank) so the first
+// read asks L2 to keep them; the re-read and the scattered stores are streaming.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ldg_v4_hint(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_hint(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t ldg_hint(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void stg_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_hint(uint64_t* p, uint64_t v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Phase 2 for one chunk.  FULL: all BLOCK*IPT keys valid (no bounds checks).
+// SAFE: rank with __match_any_sync instead of relying on the lane order of
+// same-address shared atomics (used only if the load-time self-test fails).
+template <bool FULL, bool SAFE, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
+__device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restrict__ csrc,
+                                               const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
+                                               K* __restrict__ dst, uint64_t cbase, uint32_t valid, bool gen_iota,
+                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol_stream) {
+    const int tid = threadIdx.x;
+    const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
+    const K* wsrc = csrc + wofs;
+    K key[IPT];
+    uint32_t val[VALS ? IPT : 1];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+        key[i] = (FULL || wofs + i * 32u < valid) ? ldg_hint(wsrc + i * 32, pol_stream) : static_cast<K>(0);
+    if (VALS) {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i)
+            val[i] = gen_iota ? static_cast<uint32_t>(cbase + wofs + i * 32u)
+                              : ((FULL || wofs + i * 32u < valid) ? ldg_stream(vsrc + cbase + wofs + i * 32u) : 0u);
+    }
+    uint32_t* wc = sm.cnt[c][warp];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        if (FULL || wofs + i * 32u < valid) {
+            const uint32_t d = dz.digit_sh(key[i], dsh);
+            uint32_t slot;
+            if (SAFE) {
+                const uint32_t peers = __match_any_sync(__activemask(), d);
+                const uint32_t below = __popc(peers & lanemask_lt());
+                uint32_t old = 0;
+                if (below == 0) old = atomicAdd(&wc[d], static_cast<uint32_t>(__popc(peers)));
+                slot = __shfl_sync(peers, old, __ffs(peers) - 1) + below;
+            } else {
+                slot = atomicAdd(&wc[d], 1u);
+            }
+            sm.keys[slot] = key[i];
+            if (VALS) sm.vals[slot] = val[i];
+            if (!Dz::kCheapDigit) sm.digits[slot] = static_cast<uint8_t>(d);
+        }
+    }
+    __syncthreads();
+    // coalesced scatter: consecutive slots with equal digit -> consecutive addresses
+    const uint32_t* ob = sm.out_base[c];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const uint32_t j = static_cast<uint32_t>(tid) + i * BLOCK;
+        if (FULL || j < valid) {
+            const K k = sm.keys[j];
+            const uint32_t d = Dz::kCheapDigit ? dz.digit_sh(k, dsh) : static_cast<uint32_t>(sm.digits[j]);
+            const uint32_t g = ob[d] + j;
+            stg_hint(dst + g, k, pol_stream);
+            if (VALS) stg_hint(vdst + g, sm.vals[j], pol_stream);
+        }
+    }
+    __syncthreads();
+}
+
+template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE>
+__global__ void __launch_bounds__(BLOCK, 2)
+    k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
+               const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
+               int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
+               uint32_t num_tiles, int slot, Dz dz) {
+    using Smem = OnesweepSmem<K, BLOCK, IPT, NCHUNK, VALS, !Dz::kCheapDigit>;
     constexpr int kWarps = Smem::kWarps;
+    constexpr int kChunk = Smem::kChunk;
     constexpr int kTile = Smem::kTile;
-    static_assert(BLOCK >= kRadix, "one thread per digit bin");
+    static_assert(BLOCK >= kRadix, "digit work uses kRadix/2 threads; block must cover it");
+    static_assert(IPT % 4 == 0 || sizeof(K) == 8, "phase-1 vector loads");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -246,126 +410,190 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep(const K* __restrict__ keys_i
     const uint32_t* vsrc = src_id == kBufIn ? vals_in : (src_id == kBufOut ? vals_out : vals_alt);
     uint32_t* vdst = dst_id == kBufOut ? vals_out : vals_alt;
     const bool gen_iota = iota_vals && slot == 0;
+    const uint32_t dsh = dz.shift_for(pos);
+    uint32_t* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
+    const bool vec = sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const uint32_t lane = lane_id();
 
-    if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
-    for (int i = tid; i < kWarps * (kRadix + 1); i += BLOCK) (&sm.warp_hist[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = sm.tile_id;
-    const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
-    const uint32_t valid = static_cast<uint32_t>((n - tile_base < static_cast<uint64_t>(kTile) ? n - tile_base : static_cast<uint64_t>(kTile)));
-    uint32_t* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
+#ifdef ISORT_PHASE_TIMING
+    long long pt1 = 0, pt2 = 0, pt3 = 0, pt_tiles = 0, pt_lb = 0, pt_pre = 0;
+#define ISORT_TICK(v) \
+    if (tid == 0) v = clock64()
+#else
+#define ISORT_TICK(v)
+#endif
+    for (;;) {
+#ifdef ISORT_PHASE_TIMING
+        long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+#endif
+        ISORT_TICK(q0);
+        if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
+        for (int i = tid; i < NCHUNK * kWarps * kRadix; i += BLOCK) (&sm.cnt[0][0][0])[i] = 0;
+        __syncthreads();
+        const uint32_t tile = sm.tile_id;
+        if (tile >= num_tiles) {
+#ifdef ISORT_PHASE_TIMING
+            if (tid == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 0, pt1);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 1, pt2);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 2, pt3);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 3, pt_tiles);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 4, pt_pre);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 5, pt_lb);
+            }
+#endif
+            return;
+        }
+        const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
+        const uint32_t tile_len = static_cast<uint32_t>(n - tile_base < static_cast<uint64_t>(kTile)
+                                                            ? n - tile_base : static_cast<uint64_t>(kTile));
 
-    // ---- load (warp-striped: item i of lane l is tile offset warp*32*IPT + i*32 + l)
-    K key[IPT];
-    uint32_t val[IPT];
-    const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
+        // ---------------- phase 1: per-(chunk, warp) digit counts
+        static_assert(NCHUNK % 2 == 0, "phase-1 loads are batched two chunks at a time");
+#pragma unroll 1
+        for (int c = 0; c < NCHUNK; c += 2) {
+            const uint32_t c0 = static_cast<uint32_t>(c) * kChunk + static_cast<uint32_t>(warp) * 32u * IPT;
+            const uint32_t c1 = c0 + kChunk;
+            uint32_t* wc0 = sm.cnt[c][warp];
+            uint32_t* wc1 = sm.cnt[c + 1][warp];
+            const K* ws = src + tile_base + c0;
+            if (vec && c1 + 32u * IPT <= tile_len) {
+                const uint4* v0 = reinterpret_cast<const uint4*>(ws);
+                const uint4* v1 = reinterpret_cast<const uint4*>(ws + kChunk);
+                uint4 x[IPT / 4], y[IPT / 4];
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const uint32_t o = wofs + i * 32u;
-        key[i] = o < valid ? ldg_stream(src + tile_base + o) : static_cast<K>(0);
-    }
-    if (VALS) {
+                for (int q = 0; q < IPT / 4; ++q) {
+                    x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
+                    y[q] = ldg_v4_hint(v1 + lane + 32 * q, pol_keep);
+                }
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const uint32_t o = wofs + i * 32u;
-            if (gen_iota)
-                val[i] = static_cast<uint32_t>(tile_base + o);
+                for (int q = 0; q < IPT / 4; ++q) {
+                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].x), dsh)], 1u);
+                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].y), dsh)], 1u);
+                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].z), dsh)], 1u);
+                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].w), dsh)], 1u);
+                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].x), dsh)], 1u);
+                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].y), dsh)], 1u);
+                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].z), dsh)], 1u);
+                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].w), dsh)], 1u);
+                }
+            } else {
+                for (uint32_t o = lane; o < 32u * IPT; o += 32) {
+                    if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
+                    if (c1 + o < tile_len) atomicAdd(&wc1[dz.digit_sh(ldg_hint(ws + kChunk + o, pol_keep), dsh)], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        ISORT_TICK(q1);
+
+        // ---------------- (kRadix threads, one digit each) totals, look-back, slot bases
+        if (tid < kRadix) {
+            const int d = tid;
+            uint32_t cc[NCHUNK], tot = 0;
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) x += sm.cnt[c][w][d];
+                cc[c] = x;
+                tot += x;
+            }
+            uint32_t excl = 0;
+#ifdef ISORT_PHASE_TIMING
+            long long la = clock64();
+#endif
+            if (tile == 0) {
+                st_relaxed_gpu(&lb[d], kFlagInc | tot);
+            } else {
+                st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagAgg | tot);
+                excl = lookback_digit(lb, tile, d);
+                st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagInc | (excl + tot));
+            }
+#ifdef ISORT_PHASE_TIMING
+            if (tid == 0) {
+                pt_lb += clock64() - la;
+                pt_pre += la - q1;
+            }
+#endif
+            uint32_t run = st->offs[pos][d] + excl;
+            uint32_t sc[NCHUNK];
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                sc[c] = warp_inclusive_scan(cc[c]);
+                if (lane == 31) sm.tot_w[c][warp] = sc[c];
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kRadix));
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                uint32_t pre = 0;
+#pragma unroll
+                for (int w = 0; w < kRadix / 32; ++w) pre += w < warp ? sm.tot_w[c][w] : 0u;
+                uint32_t base = pre + sc[c] - cc[c];  // chunk-local start of digit d
+                sm.out_base[c][d] = run - base;
+                run += cc[c];
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {  // per-warp slot bases for phase 2
+                    const uint32_t v = sm.cnt[c][w][d];
+                    sm.cnt[c][w][d] = base;
+                    base += v;
+                }
+            }
+        }
+        __syncthreads();
+        ISORT_TICK(q2);
+
+        // ---------------- phase 2: stage by slot, coalesced scatter
+#pragma unroll 1
+        for (int c = 0; c < NCHUNK; ++c) {
+            const uint32_t c0 = static_cast<uint32_t>(c) * kChunk;
+            if (c0 >= tile_len) break;
+            const uint32_t valid = tile_len - c0 < static_cast<uint32_t>(kChunk) ? tile_len - c0 : kChunk;
+            const uint64_t cbase = tile_base + c0;
+            if (valid == static_cast<uint32_t>(kChunk))
+                onesweep_chunk<true, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase, valid,
+                                                                    gen_iota, dsh, dz, warp, lane, pol_stream);
             else
-                val[i] = o < valid ? ldg_stream(vsrc + tile_base + o) : 0u;
+                onesweep_chunk<false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                                                                     valid, gen_iota, dsh, dz, warp, lane, pol_stream);
         }
+        ISORT_TICK(q3);
+#ifdef ISORT_PHASE_TIMING
+        pt1 += q1 - q0;
+        pt2 += q2 - q1;
+        pt3 += q3 - q2;
+        pt_tiles += 1;
+#endif
     }
+}
 
-    // ---- warp-level stable ranking: items in (i, lane) order == input order
-    uint32_t rank[IPT], dg[IPT];
-    uint32_t* wh = sm.warp_hist[warp];
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const uint32_t o = wofs + i * 32u;
-        const uint32_t d = o < valid ? dz.digit(key[i], pos) : static_cast<uint32_t>(kRadix);
-        dg[i] = d;
+// Load-time check of the property the fast rank relies on: lanes of one warp
+// instruction that add to the same shared word observe old values in ascending
+// lane order.  Adversarial patterns: 1..32 distinct words, packed 16-bit halves.
+__global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations, uint32_t seed) {
+    __shared__ uint32_t h[32][129];
+    uint32_t* wh = h[threadIdx.x >> 5];
+    const uint32_t lane = lane_id();
+    uint32_t v = seed ^ (blockIdx.x * 7919u) ^ ((threadIdx.x >> 5) * 104729u);
+    uint32_t bad = 0;
+    for (int t = 0; t < 512; ++t) {
+        for (int i = lane; i < 129; i += 32) wh[i] = 0;
+        __syncwarp();
+        v = v * 1664525u + 1013904223u;
+        const uint32_t mod = 1u + ((v >> 8) & 31u);
+        const uint32_t d = (lane * 2654435761u + v) % mod * 7u % 256u;
+        const uint32_t sh = (d >> 7) << 4;
+        const uint32_t old = (atomicAdd(&wh[d & 127], 1u << sh) >> sh) & 0xffffu;
         const uint32_t peers = __match_any_sync(ISORT_FULL_MASK, d);
-        const int leader = 31 - __clz(peers);
-        uint32_t b = 0;
-        if (static_cast<int>(lane) == leader) {
-            b = wh[d];
-            wh[d] = b + __popc(peers);
-        }
-        b = __shfl_sync(ISORT_FULL_MASK, b, leader);
-        rank[i] = b + __popc(peers & lt);
+        bad += (old != static_cast<uint32_t>(__popc(peers & lanemask_lt())));
         __syncwarp();
     }
-    __syncthreads();
-
-    // ---- per-digit: exclusive prefix over warps (in place), tile count
-    uint32_t count = 0;
-    if (tid < kRadix) {
-#pragma unroll 4
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = sm.warp_hist[w][tid];
-            sm.warp_hist[w][tid] = count;
-            count += c;
-        }
-        // publish this tile's aggregate as early as possible
-        st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + tid], (tile == 0 ? kFlagInc : kFlagAgg) | count);
-        const uint32_t inc = warp_inclusive_scan(count);
-        if (lane == 31) sm.scan_tot[tid >> 5] = inc;
-        sm.tile_start[tid] = inc - count;  // warp-local for now
-    }
-    __syncthreads();
-    if (tid < kRadix) {
-        uint32_t pre = 0;
-        for (int w = 0; w < (tid >> 5); ++w) pre += sm.scan_tot[w];
-        const uint32_t start = sm.tile_start[tid] + pre;
-        sm.tile_start[tid] = start;
-        for (int w = 0; w < kWarps; ++w) sm.warp_hist[w][tid] += start;
-
-        // ---- decoupled look-back over preceding tiles
-        uint32_t excl = 0;
-        if (tile > 0) {
-            int t = static_cast<int>(tile) - 1;
-            for (;;) {
-                const uint32_t s = ld_relaxed_gpu(&lb[static_cast<size_t>(t) * kRadix + tid]);
-                if ((s & kFlagMask) == 0) continue;
-                excl += s & kValueMask;
-                if (s & kFlagInc) break;
-                --t;
-            }
-            st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + tid], kFlagInc | (excl + count));
-        }
-        sm.out_base[tid] = st->offs[pos][tid] + excl - start;
-    }
-    __syncthreads();
-
-    // ---- stage the tile in digit order
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const uint32_t o = wofs + i * 32u;
-        if (o < valid) {
-            const uint32_t p = sm.warp_hist[warp][dg[i]] + rank[i];
-            sm.keys[p] = key[i];
-            if (VALS) sm.vals[p] = val[i];
-            if (!Dz::kCheapDigit) sm.digits[p] = static_cast<uint8_t>(dg[i]);
-        }
-    }
-    __syncthreads();
-
-    // ---- coalesced scatter: consecutive j with equal digit -> consecutive addresses
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const uint32_t j = static_cast<uint32_t>(tid) + i * BLOCK;
-        if (j < valid) {
-            const K k = sm.keys[j];
-            const uint32_t d = Dz::kCheapDigit ? dz.digit(k, pos) : static_cast<uint32_t>(sm.digits[j]);
-            const uint32_t g = sm.out_base[d] + j;
-            dst[g] = k;
-            if (VALS) vdst[g] = sm.vals[j];
-        }
-    }
+    if (bad) atomicAdd(violations, bad);
 }
 
 // ------------------------------------------------------------------- K4
