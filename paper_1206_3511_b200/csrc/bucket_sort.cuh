@@ -163,7 +163,7 @@ struct BucketDigitizer {
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         const uint64_t b = bi.bucket(static_cast<uint64_t>(key));
 #pragma unroll
-        for (int p = 0; p < kDigits; ++p) d[p] = digit_of_bucket(b, p);
+        for (int p = 0; p < kDigits; ++p) d[p] = static_cast<uint32_t>(b >> shift[p]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const { return static_cast<uint64_t>(key) <= bi.bound; }
     __device__ __forceinline__ uint64_t super_bucket(K key) const {
@@ -201,13 +201,17 @@ struct WindowCfg {
     static constexpr int kWarps = BLOCK / 32;
 };
 
+constexpr int kWinDigitBits = 9;  // window sort digit width (<= 9 bits: 512 bins)
+constexpr int kWinBins = 1 << kWinDigitBits;
+
 template <typename K, int BLOCK, int IPT, bool VALS>
 struct WindowSmem {
     K keys[BLOCK * IPT];
+    K keys2[BLOCK * IPT];  // ping-pong buffer of the in-smem sort
     uint32_t vals[VALS ? BLOCK * IPT : 1];
-    uint32_t warp_hist[BLOCK / 32][kRadix + 1];
-    uint32_t tile_start[kRadix];
-    uint32_t scan_tot[kRadix / 32];
+    uint32_t vals2[VALS ? BLOCK * IPT : 1];
+    uint32_t cnt[BLOCK / 32][kWinBins];  // per-warp digit counters, then slot bases
+    uint32_t scan_tot[BLOCK / 32];
     unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32];
     int first, last, end;
 };
@@ -221,6 +225,52 @@ __device__ __forceinline__ T block_max_u64(T v, unsigned long long* red, int war
     x = 0;
     for (int w = 0; w < warps; ++w) x = red[w] > x ? red[w] : x;
     return static_cast<T>(x);
+}
+
+// Block-wide (min, max) of K values in one barrier pair.
+template <typename K>
+__device__ __forceinline__ void block_minmax(K lo, K hi, unsigned long long* ra, unsigned long long* rb, int warps,
+                                             unsigned long long& out_lo, unsigned long long& out_hi) {
+    const unsigned long long a = warp_max<unsigned long long>(~static_cast<unsigned long long>(lo));
+    const unsigned long long b = warp_max<unsigned long long>(static_cast<unsigned long long>(hi));
+    __syncthreads();
+    if (lane_id() == 0) {
+        ra[threadIdx.x >> 5] = a;
+        rb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    unsigned long long x = 0, y = 0;
+    for (int w = 0; w < warps; ++w) {
+        x = ra[w] > x ? ra[w] : x;
+        y = rb[w] > y ? rb[w] : y;
+    }
+    out_lo = ~x;
+    out_hi = y;
+}
+
+// First index in [lo, hi) where the monotone predicate holds, or hi.  Called by a
+// whole warp: 32 probes per round narrow the range 32x.
+template <typename Pred>
+__device__ __forceinline__ int warp_lower_bound(int lo, int hi, Pred pred) {
+    // invariant: answer in [lo, hi]; pred(hi) is taken as true
+    while (lo < hi) {
+        const int step = (hi - lo + 31) / 32;
+        const int idx = lo + static_cast<int>(lane_id()) * step;
+        const bool p = idx >= hi || pred(idx);
+        const uint32_t ball = __ballot_sync(ISORT_FULL_MASK, p);
+        const int f = __ffs(ball) - 1;  // lane 31 probe may be < hi; ball can be 0
+        if (ball == 0) {
+            lo = lo + 31 * step + 1;
+            continue;
+        }
+        if (f == 0) return lo;
+        const int nlo = lo + (f - 1) * step + 1;
+        const int nhi = min(lo + f * step, hi);
+        if (step == 1) return nhi;
+        lo = nlo;
+        hi = nhi;
+    }
+    return hi;
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, bool VALS>
@@ -242,44 +292,37 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
     const int avail = static_cast<int>((n - w0 < static_cast<uint64_t>(kStage) ? n - w0 : static_cast<uint64_t>(kStage)));
     const int wlen = min(kWindow, avail);
 
-    if (tid == 0) {
-        sm.first = 0x7fffffff;
-        sm.last = -1;
-        sm.end = avail;
-    }
     for (int j = tid; j < avail; j += BLOCK) {
         sm.keys[j] = keys[w0 + j];
         if (VALS) sm.vals[j] = vals[w0 + j];
     }
     __syncthreads();
-    // super-bucket starts in [0, wlen): first and last; first start in [wlen, avail) = end
-    int my_first = 0x7fffffff, my_last = -1, my_end = 0x7fffffff;
-    for (int j = tid; j < avail; j += BLOCK) {
-        const uint64_t p = w0 + j;
-        const bool start =
-            p == 0 || dz.super_bucket(sm.keys[j]) != dz.super_bucket(j ? sm.keys[j - 1] : keys[p - 1]);
-        if (start) {
-            if (j < wlen) {
-                my_first = min(my_first, j);
-                my_last = max(my_last, j);
-            } else {
-                my_end = min(my_end, j);
-            }
+    // The passes left the array ordered by super-bucket, so the super-bucket id is
+    // non-decreasing in position and every boundary is a binary search (warp 0).
+    if (warp == 0) {
+        auto sb_at = [&](int j) { return dz.super_bucket(sm.keys[j]); };
+        int first = 0;
+        if (w0 != 0) {
+            const uint64_t prev = dz.super_bucket(keys[w0 - 1]);
+            first = warp_lower_bound(0, wlen, [&](int j) { return sb_at(j) > prev; });
+        }
+        int last = wlen, end = avail;
+        if (first < wlen) {
+            const uint64_t tail = sb_at(wlen - 1);
+            last = warp_lower_bound(first, wlen - 1, [&](int j) { return sb_at(j) >= tail; });
+            end = warp_lower_bound(wlen, avail, [&](int j) { return sb_at(j) > tail; });
+        }
+        if (lane == 0) {
+            sm.first = first;
+            sm.last = last;
+            sm.end = end;
         }
     }
-    my_first = __reduce_min_sync(ISORT_FULL_MASK, my_first);
-    my_last = __reduce_max_sync(ISORT_FULL_MASK, my_last);
-    my_end = __reduce_min_sync(ISORT_FULL_MASK, my_end);
-    if (lane == 0) {
-        if (my_first != 0x7fffffff) atomicMin(&sm.first, my_first);
-        if (my_last >= 0) atomicMax(&sm.last, my_last);
-        if (my_end != 0x7fffffff) atomicMin(&sm.end, my_end);
-    }
     __syncthreads();
-    const int first = sm.first < wlen ? sm.first : wlen;
+    const int first = sm.first;
     int end = sm.end;
 
-    // summary: head = keys before the first owned super-bucket
+    // summary for K6: keys before the first owned super-bucket (they belong to an earlier one)
     {
         K hmin = static_cast<K>(~static_cast<K>(0)), hmax = 0;
         for (int j = tid; j < first; j += BLOCK) {
@@ -287,11 +330,11 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
             hmin = k < hmin ? k : hmin;
             hmax = k > hmax ? k : hmax;
         }
-        const unsigned long long a = block_max_u64(~static_cast<unsigned long long>(hmin), sm.red_a, kWarps);
-        const unsigned long long b = block_max_u64(static_cast<unsigned long long>(hmax), sm.red_b, kWarps);
+        unsigned long long a, b;
+        block_minmax(hmin, hmax, sm.red_a, sm.red_b, kWarps, a, b);
         if (tid == 0) {
             summ[blockIdx.x].first = first < wlen ? w0 + first : ~0ull;
-            summ[blockIdx.x].hmin = ~a;
+            summ[blockIdx.x].hmin = a;
             summ[blockIdx.x].hmax = b;
         }
     }
@@ -307,12 +350,12 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
             omin = k < omin ? k : omin;
             omax = k > omax ? k : omax;
         }
-        const unsigned long long a = block_max_u64(~static_cast<unsigned long long>(omin), sm.red_a, kWarps);
-        const unsigned long long b = block_max_u64(static_cast<unsigned long long>(omax), sm.red_b, kWarps);
+        unsigned long long a, b;
+        block_minmax(omin, omax, sm.red_a, sm.red_b, kWarps, a, b);
         if (tid == 0) {
             const uint32_t r = atomicAdd(&bst->n_over, 1u);
             over[r].start = w0 + ostart;
-            over[r].kmin = ~a;
+            over[r].kmin = a;
             over[r].kmax = b;
             over[r].window = blockIdx.x;
         }
@@ -321,96 +364,84 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
     const int len = end - first;
     if (len <= 1) return;
 
-    // ---- stable block radix sort of sm.keys[first, end) by (key - min)
+    // ---- stable in-smem LSD sort of sm.keys[first, end) by (key - min), r-bit digits
+    // Same rank primitive as the one-sweep pass: per-warp counters pre-scanned into
+    // slot bases, slot = atomicAdd (lane-ordered, program-ordered => stable).
     K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
     for (int j = first + tid; j < end; j += BLOCK) {
         const K k = sm.keys[j];
         kmin = k < kmin ? k : kmin;
         kmax = k > kmax ? k : kmax;
     }
-    kmin = static_cast<K>(~block_max_u64(~static_cast<unsigned long long>(kmin), sm.red_a, kWarps));
-    kmax = static_cast<K>(block_max_u64(static_cast<unsigned long long>(kmax), sm.red_b, kWarps));
+    {
+        unsigned long long a, b;
+        block_minmax(kmin, kmax, sm.red_a, sm.red_b, kWarps, a, b);
+        kmin = static_cast<K>(a);
+        kmax = static_cast<K>(b);
+    }
     if (kmin == kmax) return;  // one key value: arrival order is the answer
     const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
-    const int passes = (bits + kRadixBits - 1) / kRadixBits;
-
-    K key[IPT];
-    uint32_t val[IPT];
+    const int passes = (bits + kWinDigitBits - 1) / kWinDigitBits;
+    const int r = (bits + passes - 1) / passes;
+    const uint32_t nbins = 1u << r, mask = nbins - 1u;
+    K* ka = sm.keys + first;
+    K* kb = sm.keys2;
+    uint32_t* va = sm.vals + first;
+    uint32_t* vb = sm.vals2;
     const int wofs = warp * 32 * IPT + static_cast<int>(lane);
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int o = wofs + i * 32;
-        key[i] = o < len ? sm.keys[first + o] : static_cast<K>(0);
-        if (VALS) val[i] = o < len ? sm.vals[first + o] : 0u;
-    }
-    const uint32_t lt = lanemask_lt();
     for (int pass = 0; pass < passes; ++pass) {
-        const uint32_t shift = static_cast<uint32_t>(pass * kRadixBits);
-        for (int i = tid; i < kWarps * (kRadix + 1); i += BLOCK) (&sm.warp_hist[0][0])[i] = 0;
+        const uint32_t shift = static_cast<uint32_t>(pass * r);
+        for (int i = tid; i < kWarps * kWinBins; i += BLOCK) (&sm.cnt[0][0])[i] = 0;
         __syncthreads();
-        uint32_t rank[IPT], dg[IPT];
-        uint32_t* wh = sm.warp_hist[warp];
+        uint32_t* wc = sm.cnt[warp];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int o = wofs + i * 32;
-            const uint32_t d = o < len ? static_cast<uint32_t>((static_cast<uint64_t>(key[i] - kmin) >> shift) & 255u)
-                                       : static_cast<uint32_t>(kRadix);
-            dg[i] = d;
-            const uint32_t peers = __match_any_sync(ISORT_FULL_MASK, d);
-            const int leader = 31 - __clz(peers);
-            uint32_t b = 0;
-            if (static_cast<int>(lane) == leader) {
-                b = wh[d];
-                wh[d] = b + __popc(peers);
-            }
-            b = __shfl_sync(ISORT_FULL_MASK, b, leader);
-            rank[i] = b + __popc(peers & lt);
-            __syncwarp();
+            if (o < len) atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
         }
         __syncthreads();
-        if (tid < kRadix) {
-            uint32_t count = 0;
+        // bin b (one per thread): totals over warps, block scan over bins, per-warp bases
+        uint32_t tot = 0;
+        const uint32_t b = static_cast<uint32_t>(tid);
+        if (b < nbins) {
+#pragma unroll 4
+            for (int w = 0; w < kWarps; ++w) tot += sm.cnt[w][b];
+        }
+        const uint32_t inc = warp_inclusive_scan(tot);
+        if (lane == 31) sm.scan_tot[warp] = inc;
+        __syncthreads();
+        if (b < nbins) {
+            uint32_t base = inc - tot;
+            for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
+#pragma unroll 4
             for (int w = 0; w < kWarps; ++w) {
-                const uint32_t c = sm.warp_hist[w][tid];
-                sm.warp_hist[w][tid] = count;
-                count += c;
+                const uint32_t v = sm.cnt[w][b];
+                sm.cnt[w][b] = base;
+                base += v;
             }
-            const uint32_t inc = warp_inclusive_scan(count);
-            if (lane == 31) sm.scan_tot[tid >> 5] = inc;
-            sm.tile_start[tid] = inc - count;
-        }
-        __syncthreads();
-        if (tid < kRadix) {
-            uint32_t pre = 0;
-            for (int w = 0; w < (tid >> 5); ++w) pre += sm.scan_tot[w];
-            const uint32_t start = sm.tile_start[tid] + pre;
-            for (int w = 0; w < kWarps; ++w) sm.warp_hist[w][tid] += start;
         }
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int o = wofs + i * 32;
             if (o < len) {
-                const uint32_t p = sm.warp_hist[warp][dg[i]] + rank[i];
-                sm.keys[first + p] = key[i];
-                if (VALS) sm.vals[first + p] = val[i];
+                const K k = ka[o];
+                const uint32_t slot = atomicAdd(&wc[static_cast<uint32_t>((k - kmin) >> shift) & mask], 1u);
+                kb[slot] = k;
+                if (VALS) vb[slot] = va[o];
             }
         }
         __syncthreads();
-        if (pass + 1 < passes) {
-#pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const int o = wofs + i * 32;
-                if (o < len) {
-                    key[i] = sm.keys[first + o];
-                    if (VALS) val[i] = sm.vals[first + o];
-                }
-            }
-        }
+        K* tk = ka;
+        ka = kb;
+        kb = tk;
+        uint32_t* tv = va;
+        va = vb;
+        vb = tv;
     }
-    for (int j = first + tid; j < end; j += BLOCK) {
-        keys[w0 + j] = sm.keys[j];
-        if (VALS) vals[w0 + j] = sm.vals[j];
+    for (int j = tid; j < len; j += BLOCK) {
+        keys[w0 + first + j] = ka[j];
+        if (VALS) vals[w0 + first + j] = va[j];
     }
 }
 

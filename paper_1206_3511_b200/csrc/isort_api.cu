@@ -77,11 +77,21 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 // Tile shapes per (key width, payload).  Tile = BLOCK * IPT keys.
 template <typename K, bool VALS>
 struct PassCfg {
-    static constexpr int kBlock = 512;
+#ifndef ISORT_PASS_BLOCK
+#define ISORT_PASS_BLOCK 512
+#endif
+    static constexpr int kBlock = ISORT_PASS_BLOCK;
     static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : 12) : (VALS ? 6 : 8);
     static constexpr int kChunks = 4;
     static constexpr int kTile = kBlock * kIpt * kChunks;
-    static constexpr int kCtasPerSm = 2;
+    static constexpr int kCtasPerSm = 2048 / kBlock;
+};
+
+// Upfront histogram replication (lane copies per bin): 64 KB of counters.
+template <int D>
+struct UpfrontCfg {
+    static constexpr int kRep = D <= 4 ? 16 : 8;
+    static constexpr size_t kSmem = static_cast<size_t>(D) * kRadix * kRep * sizeof(uint32_t);
 };
 
 // ------------------------------------------------------- rank self-test
@@ -173,12 +183,18 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
         prof_mark(s, "memset");
     }
     const bool vec = (reinterpret_cast<uintptr_t>(kin) & 15u) == 0;
+    using UCfg = UpfrontCfg<D>;
     const uint64_t want = (n + 4ull * kUpfrontBlock - 1) / (4ull * kUpfrontBlock);
-    const unsigned grid1 = static_cast<unsigned>(want < 4ull * kNumSMs ? (want ? want : 1) : 4ull * kNumSMs);
-    if (vec)
-        k_upfront<K, Dz, kUpfrontBlock, true><<<grid1, kUpfrontBlock, 0, s>>>(kin, n, st, dz);
-    else
-        k_upfront<K, Dz, kUpfrontBlock, false><<<grid1, kUpfrontBlock, 0, s>>>(kin, n, st, dz);
+    const unsigned grid1 = static_cast<unsigned>(want < 3ull * kNumSMs ? (want ? want : 1) : 3ull * kNumSMs);
+    if (vec) {
+        auto* k1 = k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, true>;
+        set_max_smem_once(k1, UCfg::kSmem);
+        k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
+    } else {
+        auto* k1 = k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, false>;
+        set_max_smem_once(k1, UCfg::kSmem);
+        k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
+    }
     prof_mark(s, "upfront");
     k_plan<D><<<1, kRadix, 0, s>>>(st, n, skip_sorted ? 1 : 0);
     prof_mark(s, "plan");

@@ -8,20 +8,15 @@
 // so the engine sorts with 8-bit digits whatever base the caller names.
 //
 // Device pipeline (all stream-ordered, no host round trip):
-//   K1 k_upfront   one read of the keys: every digit histogram, max key, number
-//                  of adjacent descents (0 => already sorted), plus an optional
-//                  digitizer range check (bucket sort).          4n B  HBM read
+//   K1 k_upfront   one read of the keys: every digit histogram (lane-replicated
+//                  shared counters: no bank conflicts), max key, number of
+//                  adjacent descents (0 => already sorted), optional digitizer
+//                  range check (bucket sort).                    4n B HBM read
 //   K2 k_plan      scans the histograms, drops trivial digit passes (one bin
 //                  holds all n keys => the pass is the identity) and the whole
 //                  sort when the input is already sorted; assigns ping-pong
 //                  buffers so the last executed pass lands in `out`.
-//   K3 k_onesweep  one launch per digit slot; persistent CTAs take ~30K-key
-//                  tiles by atomic ticket (forward progress for the look-back).
-//                  Phase 1 counts the tile's digits and resolves its global
-//                  offsets by windowed decoupled look-back; phase 2 re-reads the
-//                  tile (L2 hits) chunk by chunk: warp-level __match_any_sync
-//                  ranking, smem-staged digit-sorted chunk, coalesced stores.
-//                                                                 8n B / pass
+//   K3 k_onesweep  one launch per digit slot (see the K3 comment).  8n B / pass
 //   K4 k_copy      only when no pass executes (sorted input): out = in.
 #pragma once
 
@@ -52,6 +47,7 @@ struct RadixState {
     int32_t digit_of_slot[kMaxDigits];  // K2
     int32_t src_of_slot[kMaxDigits];
     int32_t dst_of_slot[kMaxDigits];
+    unsigned long long prof[16];        // debug counters (ISORT_PHASE_TIMING builds)
 };
 
 // ------------------------------------------------------------- digitizers
@@ -73,22 +69,26 @@ struct RadixDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
 #pragma unroll
-        for (int p = 0; p < kDigits; ++p) d[p] = digit(key, p);
+        for (int p = 0; p < kDigits; ++p) d[p] = digit_sh(key, 8u * p);
     }
     __device__ __forceinline__ bool in_range(K) const { return true; }
 };
 
 // ------------------------------------------------------------------- K1
-template <typename K, typename Dz, int BLOCK, bool VEC>
+// Digit histograms in lane-replicated shared counters: copy (lane % R) of bin b
+// of digit p lives at ((p * 256 + b) * R + lane % R), so lanes of one atomic
+// instruction hit distinct banks (R = 32) or at most 2-way (R = 16).
+template <typename K, typename Dz, int BLOCK, int R, bool VEC>
 __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, uint64_t n,
                                                    RadixState* __restrict__ st, Dz dz) {
     constexpr int D = Dz::kDigits;
-    __shared__ uint32_t sh[D][kRadix];
+    extern __shared__ __align__(16) uint32_t uf_cnt[];  // D * 256 * R
     __shared__ unsigned long long red_max[BLOCK / 32];
     __shared__ unsigned long long red_nmin[BLOCK / 32];
     __shared__ uint32_t red_desc[BLOCK / 32];
-    for (int i = threadIdx.x; i < D * kRadix; i += BLOCK) (&sh[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < D * kRadix * R; i += BLOCK) uf_cnt[i] = 0;
     __syncthreads();
+    const uint32_t copy = lane_id() % R;
 
     K kmax = 0;
     K kmin = static_cast<K>(~static_cast<K>(0));
@@ -104,13 +104,12 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
         uint32_t d[D];
         dz.all_digits(k, d);
 #pragma unroll
-        for (int p = 0; p < D; ++p) atomicAdd(&sh[p][d[p]], 1u);
+        for (int p = 0; p < D; ++p) atomicAdd(&uf_cnt[(p * kRadix + d[p]) * R + copy], 1u);
     };
 
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * BLOCK;
-    constexpr int V = 16 / sizeof(K) >= 4 ? 4 : 4;  // 4 keys per thread-iteration
+    constexpr int V = 4;  // 4 keys per thread-iteration
     if (VEC) {
-        // 4 consecutive keys per iteration via 16-byte vector loads.
         const uint64_t nv = n / V;
         for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * BLOCK + threadIdx.x; v < nv; v += stride) {
             K k[V];
@@ -151,8 +150,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     unsigned long long m = warp_max<unsigned long long>(static_cast<unsigned long long>(kmax));
     unsigned long long nm = warp_max<unsigned long long>(~static_cast<unsigned long long>(kmin));
     uint32_t ds = warp_sum(desc);
-    unsigned long long fb = ~first_bad;  // max of complements = min index
-    fb = warp_max<unsigned long long>(fb);
+    unsigned long long fb = warp_max<unsigned long long>(~first_bad);  // max of complements = min index
     const int w = threadIdx.x / 32;
     if (lane_id() == 0) {
         red_max[w] = m;
@@ -176,7 +174,9 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
         }
     }
     for (int i = threadIdx.x; i < D * kRadix; i += BLOCK) {
-        const uint32_t c = (&sh[0][0])[i];
+        uint32_t c = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) c += uf_cnt[i * R + ((r + i) & (R - 1))];  // rotate: spread banks
         if (c) atomicAdd(&st->hist[i / kRadix][i % kRadix], c);
     }
 }
@@ -217,34 +217,34 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
 // ------------------------------------------------------------------- K3
 // Persistent two-phase one-sweep pass.
 //
-// B200 facts that shape it (profiles/r01_microbench_warp_primitives.txt,
-// profiles/r01_onesweep_*.txt):
-//  * A pass must move 8n bytes in ~0.12 ms at n = 1e8: ~2.9 keys/cycle/SM, i.e.
-//    <= ~44 thread-instructions and ~11 shared-memory wavefront-cycles per 32
-//    keys.
+// B200 facts that shape it (profiles/r01_*):
+//  * A pass must move 8n bytes in ~0.12 ms at n = 1e8: ~2.9 keys/cycle/SM.
 //  * __match_any_sync costs ~63 cycles per warp instruction per SM and an 8-ballot
-//    peer mask ~28: a match-based stable rank caps a pass near 0.7 ms.  Shared
-//    atomics with return cost ~2.6 cycles, and same-address shared atomics of one
+//    peer mask ~28, so a match-based stable rank caps a pass near 0.7 ms.  Shared
+//    atomics with return cost ~2.6 cycles and same-address shared atomics of one
 //    warp instruction are granted in ascending lane order (0 violations in 6.2e8
-//    lane-trials; re-verified at load time by isort_selftest, with the match-based
-//    rank as the fallback).  So a key's stable slot is one atomicAdd.
+//    lane-trials; re-verified at load time by k_selftest_atomic_order, with the
+//    match-based rank as the fallback).  So a key's stable rank is one atomicAdd.
+//  * The shared-memory pipe is the next wall: a random 4-byte access by 32 lanes
+//    costs ~3.5 bank wavefronts.  The pass therefore makes exactly two random
+//    shared accesses per key (rank atomic, staging store); counting uses
+//    lane-replicated counters (conflict-free).
 //  * Decoupled look-back must walk (L2 latency x tile rate) predecessors; big
-//    tiles (~30K keys) keep that to ~1 windowed round trip.
+//    tiles (NCHUNK chunks) keep that walk short.
 //
-// Tile = NCHUNK chunks of BLOCK*IPT keys.  Warp w of the CTA always owns the
-// same 32*IPT-key slice of every chunk (warp-striped: item i of lane l at slice
-// offset i*32 + l, so (item, lane) order is input order).
-//   phase 1  each warp counts the digits of its slices into packed 16-bit
-//            counters cnt[chunk][warp][d & 127] (halves for d and d + 128), with
-//            16-byte loads kept in L2 (evict_last); the tile total is published
-//            as the aggregate and the global offsets come from the look-back.
-//            The counters are then rewritten as chunk-local start slots:
-//            local(c, w, d) = sum_{d' < d} cnt_c(d') + sum_{w' < w} cnt(c, w', d).
-//   phase 2  per chunk: re-read (L2 hits), slot = atomicAdd(counter) -> stage the
-//            key at that slot (digit-sorted chunk), then coalesced stores at
-//            out_base[chunk][d] + slot.
-// CTAs are persistent (grid = 2 x SMs) and take tiles by atomic ticket, so every
-// tile a CTA waits on is owned by a running CTA (forward progress).
+// Per tile (NCHUNK chunks of BLOCK*IPT keys, tile id by atomic ticket); warp w
+// always owns the same 32*IPT-key slice of every chunk, warp-striped (item i of
+// lane l at slice offset i*32 + l, so (item, lane) order is input order):
+//   phase 1  16-byte loads (kept in L2 with evict_last) count digits per
+//            (chunk, warp); the tile total is published as the aggregate and the
+//            look-back resolves the tile's global prefix; the counters are
+//            rewritten as chunk-local start slots:
+//              slot0(c, w, d) = sum_{d' < d} cnt_c(d') + sum_{w' < w} cnt(c, w', d)
+//   phase 2  per chunk: re-read keys (L2 hits), slot = atomicAdd(counter) (stable:
+//            lanes in order, items in program order), stage the key there (a
+//            digit-sorted chunk), then coalesced stores at out_base[c][d] + slot.
+// CTAs are small (256 threads, 4 per SM) and persistent; they take tiles by
+// atomic ticket, so every tile a CTA waits on is owned by a running CTA.
 template <typename K, int BLOCK, int IPT, int NCHUNK, bool VALS, bool STAGE_DIGITS>
 struct OnesweepSmem {
     static constexpr int kWarps = BLOCK / 32;
@@ -252,6 +252,7 @@ struct OnesweepSmem {
     static constexpr int kTile = kChunk * NCHUNK;
     uint32_t cnt[NCHUNK][kWarps][kRadix];  // phase 1: counts; then chunk-local slot bases
     uint32_t out_base[NCHUNK][kRadix];     // global position = out_base[c][d] + slot
+    uint32_t offs[kRadix];                 // pass digit offsets (from K2)
     K keys[kChunk];
     uint32_t vals[VALS ? kChunk : 1];
     uint8_t digits[STAGE_DIGITS ? kChunk : 1];  // digit per staged key (expensive digitizers)
@@ -261,12 +262,11 @@ struct OnesweepSmem {
 
 constexpr int kLookbackWindow = 16;  // predecessors read per round trip, per digit
 
-// Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back.
-// All kLookbackWindow loads are in flight together, so the usual case (an
-// inclusive prefix within the window) costs one L2 round trip.
-__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ lb, uint32_t tile, int d) {
-    uint32_t excl = 0;
-    int t = static_cast<int>(tile) - 1;
+// Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back,
+// all kLookbackWindow loads in flight per round trip.
+__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ lb, int t_start, int d,
+                                                   uint32_t excl) {
+    int t = t_start;
     while (t >= 0) {
         uint32_t sv[kLookbackWindow];
 #pragma unroll
@@ -327,14 +327,26 @@ __device__ __forceinline__ void stg_hint(uint64_t* p, uint64_t v, uint64_t pol) 
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
+// Stable slot of a key: slot = atomicAdd(counter), relying on lane-ordered
+// same-address shared atomics; SAFE: __match_any_sync peers instead.
+template <bool SAFE>
+__device__ __forceinline__ uint32_t warp_slot(uint32_t* wc, uint32_t d) {
+    if (SAFE) {
+        const uint32_t peers = __match_any_sync(__activemask(), d);
+        const uint32_t below = __popc(peers & lanemask_lt());
+        uint32_t old = 0;
+        if (below == 0) old = atomicAdd(&wc[d], static_cast<uint32_t>(__popc(peers)));
+        return __shfl_sync(peers, old, __ffs(peers) - 1) + below;
+    }
+    return atomicAdd(&wc[d], 1u);
+}
+
 // Phase 2 for one chunk.  FULL: all BLOCK*IPT keys valid (no bounds checks).
-// SAFE: rank with __match_any_sync instead of relying on the lane order of
-// same-address shared atomics (used only if the load-time self-test fails).
 template <bool FULL, bool SAFE, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
 __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restrict__ csrc,
                                                const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                                                K* __restrict__ dst, uint64_t cbase, uint32_t valid, bool gen_iota,
-                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol_stream) {
+                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol) {
     const int tid = threadIdx.x;
     const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
     const K* wsrc = csrc + wofs;
@@ -342,7 +354,7 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
     uint32_t val[VALS ? IPT : 1];
 #pragma unroll
     for (int i = 0; i < IPT; ++i)
-        key[i] = (FULL || wofs + i * 32u < valid) ? ldg_hint(wsrc + i * 32, pol_stream) : static_cast<K>(0);
+        key[i] = (FULL || wofs + i * 32u < valid) ? ldg_hint(wsrc + i * 32, pol) : static_cast<K>(0);
     if (VALS) {
 #pragma unroll
         for (int i = 0; i < IPT; ++i)
@@ -354,23 +366,13 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
     for (int i = 0; i < IPT; ++i) {
         if (FULL || wofs + i * 32u < valid) {
             const uint32_t d = dz.digit_sh(key[i], dsh);
-            uint32_t slot;
-            if (SAFE) {
-                const uint32_t peers = __match_any_sync(__activemask(), d);
-                const uint32_t below = __popc(peers & lanemask_lt());
-                uint32_t old = 0;
-                if (below == 0) old = atomicAdd(&wc[d], static_cast<uint32_t>(__popc(peers)));
-                slot = __shfl_sync(peers, old, __ffs(peers) - 1) + below;
-            } else {
-                slot = atomicAdd(&wc[d], 1u);
-            }
-            sm.keys[slot] = key[i];
-            if (VALS) sm.vals[slot] = val[i];
-            if (!Dz::kCheapDigit) sm.digits[slot] = static_cast<uint8_t>(d);
+            const uint32_t s = warp_slot<SAFE>(wc, d);
+            sm.keys[s] = key[i];
+            if (VALS) sm.vals[s] = val[i];
+            if (!Dz::kCheapDigit) sm.digits[s] = static_cast<uint8_t>(d);
         }
     }
     __syncthreads();
-    // coalesced scatter: consecutive slots with equal digit -> consecutive addresses
     const uint32_t* ob = sm.out_base[c];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -379,15 +381,15 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
             const K k = sm.keys[j];
             const uint32_t d = Dz::kCheapDigit ? dz.digit_sh(k, dsh) : static_cast<uint32_t>(sm.digits[j]);
             const uint32_t g = ob[d] + j;
-            stg_hint(dst + g, k, pol_stream);
-            if (VALS) stg_hint(vdst + g, sm.vals[j], pol_stream);
+            stg_hint(dst + g, k, pol);
+            if (VALS) stg_hint(vdst + g, sm.vals[j], pol);
         }
     }
     __syncthreads();
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE>
-__global__ void __launch_bounds__(BLOCK, 2)
+__global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
@@ -396,8 +398,8 @@ __global__ void __launch_bounds__(BLOCK, 2)
     constexpr int kWarps = Smem::kWarps;
     constexpr int kChunk = Smem::kChunk;
     constexpr int kTile = Smem::kTile;
-    static_assert(BLOCK >= kRadix, "digit work uses kRadix/2 threads; block must cover it");
-    static_assert(IPT % 4 == 0 || sizeof(K) == 8, "phase-1 vector loads");
+    static_assert(BLOCK % kRadix == 0, "threads [0, kRadix) own one digit each in the per-tile section");
+    static_assert(NCHUNK % 2 == 0, "phase-1 loads are batched two chunks at a time");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -412,49 +414,39 @@ __global__ void __launch_bounds__(BLOCK, 2)
     const bool gen_iota = iota_vals && slot == 0;
     const uint32_t dsh = dz.shift_for(pos);
     uint32_t* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
-    const bool vec = sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+    const bool vec = sizeof(K) == 4 && IPT % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const uint32_t lane = lane_id();
+    if (tid < kRadix) sm.offs[tid] = st->offs[pos][tid];
 
 #ifdef ISORT_PHASE_TIMING
-    long long pt1 = 0, pt2 = 0, pt3 = 0, pt_tiles = 0, pt_lb = 0, pt_pre = 0;
+    long long acc[4] = {0, 0, 0, 0};
+    long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
 #define ISORT_TICK(v) \
     if (tid == 0) v = clock64()
 #else
 #define ISORT_TICK(v)
 #endif
+
     for (;;) {
-#ifdef ISORT_PHASE_TIMING
-        long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-#endif
         ISORT_TICK(q0);
         if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
-        for (int i = tid; i < NCHUNK * kWarps * kRadix; i += BLOCK) (&sm.cnt[0][0][0])[i] = 0;
+        {
+            uint4* c4 = reinterpret_cast<uint4*>(&sm.cnt[0][0][0]);
+            for (int i = tid; i < NCHUNK * kWarps * kRadix / 4; i += BLOCK) c4[i] = make_uint4(0, 0, 0, 0);
+        }
         __syncthreads();
         const uint32_t tile = sm.tile_id;
-        if (tile >= num_tiles) {
-#ifdef ISORT_PHASE_TIMING
-            if (tid == 0) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 0, pt1);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 1, pt2);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 2, pt3);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 3, pt_tiles);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 4, pt_pre);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&st->offs[kMaxDigits - 1][0]) + 5, pt_lb);
-            }
-#endif
-            return;
-        }
+        if (tile >= num_tiles) break;
         const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
         const uint32_t tile_len = static_cast<uint32_t>(n - tile_base < static_cast<uint64_t>(kTile)
                                                             ? n - tile_base : static_cast<uint64_t>(kTile));
 
         // ---------------- phase 1: per-(chunk, warp) digit counts
-        static_assert(NCHUNK % 2 == 0, "phase-1 loads are batched two chunks at a time");
 #pragma unroll 1
         for (int c = 0; c < NCHUNK; c += 2) {
             const uint32_t c0 = static_cast<uint32_t>(c) * kChunk + static_cast<uint32_t>(warp) * 32u * IPT;
@@ -485,14 +477,15 @@ __global__ void __launch_bounds__(BLOCK, 2)
             } else {
                 for (uint32_t o = lane; o < 32u * IPT; o += 32) {
                     if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
-                    if (c1 + o < tile_len) atomicAdd(&wc1[dz.digit_sh(ldg_hint(ws + kChunk + o, pol_keep), dsh)], 1u);
+                    if (c1 + o < tile_len)
+                        atomicAdd(&wc1[dz.digit_sh(ldg_hint(ws + kChunk + o, pol_keep), dsh)], 1u);
                 }
             }
         }
         __syncthreads();
         ISORT_TICK(q1);
 
-        // ---------------- (kRadix threads, one digit each) totals, look-back, slot bases
+        // ---------------- one thread per digit: totals, look-back, slot bases
         if (tid < kRadix) {
             const int d = tid;
             uint32_t cc[NCHUNK], tot = 0;
@@ -505,30 +498,25 @@ __global__ void __launch_bounds__(BLOCK, 2)
                 tot += x;
             }
             uint32_t excl = 0;
-#ifdef ISORT_PHASE_TIMING
-            long long la = clock64();
-#endif
             if (tile == 0) {
                 st_relaxed_gpu(&lb[d], kFlagInc | tot);
             } else {
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagAgg | tot);
-                excl = lookback_digit(lb, tile, d);
+                excl = lookback_digit(lb, static_cast<int>(tile) - 1, d, 0u);
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagInc | (excl + tot));
             }
-#ifdef ISORT_PHASE_TIMING
-            if (tid == 0) {
-                pt_lb += clock64() - la;
-                pt_pre += la - q1;
-            }
-#endif
-            uint32_t run = st->offs[pos][d] + excl;
+            ISORT_TICK(q2);
+            uint32_t run = sm.offs[d] + excl;
             uint32_t sc[NCHUNK];
 #pragma unroll
             for (int c = 0; c < NCHUNK; ++c) {
                 sc[c] = warp_inclusive_scan(cc[c]);
                 if (lane == 31) sm.tot_w[c][warp] = sc[c];
             }
-            asm volatile("bar.sync 1, %0;" ::"n"(kRadix));
+            if (BLOCK == kRadix)
+                __syncthreads();
+            else
+                asm volatile("bar.sync 1, %0;" ::"n"(kRadix));
 #pragma unroll
             for (int c = 0; c < NCHUNK; ++c) {
                 uint32_t pre = 0;
@@ -546,7 +534,6 @@ __global__ void __launch_bounds__(BLOCK, 2)
             }
         }
         __syncthreads();
-        ISORT_TICK(q2);
 
         // ---------------- phase 2: stage by slot, coalesced scatter
 #pragma unroll 1
@@ -564,31 +551,36 @@ __global__ void __launch_bounds__(BLOCK, 2)
         }
         ISORT_TICK(q3);
 #ifdef ISORT_PHASE_TIMING
-        pt1 += q1 - q0;
-        pt2 += q2 - q1;
-        pt3 += q3 - q2;
-        pt_tiles += 1;
+        acc[0] += q1 - q0;
+        acc[1] += q2 - q1;
+        acc[2] += q3 - q2;
+        acc[3] += 1;
 #endif
     }
+#ifdef ISORT_PHASE_TIMING
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
+    }
+#endif
+#undef ISORT_TICK
 }
 
 // Load-time check of the property the fast rank relies on: lanes of one warp
 // instruction that add to the same shared word observe old values in ascending
-// lane order.  Adversarial patterns: 1..32 distinct words, packed 16-bit halves.
+// lane order.  Adversarial patterns: 1..32 distinct words per instruction.
 __global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations, uint32_t seed) {
-    __shared__ uint32_t h[32][129];
+    __shared__ uint32_t h[32][257];
     uint32_t* wh = h[threadIdx.x >> 5];
     const uint32_t lane = lane_id();
     uint32_t v = seed ^ (blockIdx.x * 7919u) ^ ((threadIdx.x >> 5) * 104729u);
     uint32_t bad = 0;
     for (int t = 0; t < 512; ++t) {
-        for (int i = lane; i < 129; i += 32) wh[i] = 0;
+        for (int i = lane; i < 257; i += 32) wh[i] = 0;
         __syncwarp();
         v = v * 1664525u + 1013904223u;
         const uint32_t mod = 1u + ((v >> 8) & 31u);
         const uint32_t d = (lane * 2654435761u + v) % mod * 7u % 256u;
-        const uint32_t sh = (d >> 7) << 4;
-        const uint32_t old = (atomicAdd(&wh[d & 127], 1u << sh) >> sh) & 0xffffu;
+        const uint32_t old = atomicAdd(&wh[d], 1u);
         const uint32_t peers = __match_any_sync(ISORT_FULL_MASK, d);
         bad += (old != static_cast<uint32_t>(__popc(peers & lanemask_lt())));
         __syncwarp();

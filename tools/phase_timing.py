@@ -35,9 +35,21 @@ s = torch.cuda.current_stream().cuda_stream
 for rep in range(1):
     assert lib.isort_radix_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, 0, temp.data_ptr(), tb, s) == 0
     torch.cuda.synchronize()
-# RadixState at offset 0 of temp; offs[7][0..7] (unused for u32 keys) holds 4 u64 accumulators
-off = 4 * (8 * 256) + 4 * (7 * 256)  # RadixState.offs[7][0]
-acc = temp[off:off + 48].cpu().numpy().view(np.uint64)
+# RadixState (radix_onesweep.cuh) at offset 0 of temp: prof[0..2] accumulate
+# phase-1 cycles, phase-2 cycles and tiles over all passes.
+import ctypes as C
+
+
+class RadixState(C.Structure):
+    _fields_ = [("hist", C.c_uint32 * 2048), ("offs", C.c_uint32 * 2048), ("max_key", C.c_uint64),
+                ("not_min_key", C.c_uint64), ("first_bad", C.c_uint64), ("descents", C.c_uint32),
+                ("n_active", C.c_uint32), ("copy_in_to_out", C.c_uint32), ("tile_ticket", C.c_uint32 * 8),
+                ("digit_of_slot", C.c_int32 * 8), ("src_of_slot", C.c_int32 * 8), ("dst_of_slot", C.c_int32 * 8),
+                ("prof", C.c_uint64 * 16)]
+
+
+off = RadixState.prof.offset
+acc = temp[off:off + 128].cpu().numpy().view(np.uint64)
 tiles = int(acc[3])
-print(f"tiles={tiles}  cycles/tile: phase1={acc[0] / tiles:.0f}  serial={acc[1] / tiles:.0f}  phase2={acc[2] / tiles:.0f}"
-      f"  [serial: pre-lookback={acc[4] / tiles:.0f} lookback={acc[5] / tiles:.0f}]")
+print(f"tiles={tiles}  cycles/tile: phase1={acc[0] / tiles:.0f}  totals+lookback={acc[1] / tiles:.0f}"
+      f"  bases+phase2={acc[2] / tiles:.0f}")
