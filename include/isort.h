@@ -114,6 +114,19 @@ int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uin
                           void* temp, size_t temp_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Key-range partition (multi-GPU sort).  Not in the
+ * reference (single-threaded); the engine's scale-out step.
+ * Stable partition of keys_in into `parts` destination ranges: destination of
+ * a key = number of `splitters` (host array, parts - 1 ascending values) that
+ * are <= key.  keys_out holds destination 0's keys, then 1's, ... each in input
+ * order; counts (device, `parts` u64) receives the per-destination counts.
+ * ---------------------------------------------------------------------- */
+size_t isort_partition_temp_bytes(uint64_t n, int key_bytes, int vals_mode);
+int isort_partition_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                        uint32_t* vals_out, uint64_t n, const uint32_t* splitters, int parts,
+                        int vals_mode, uint64_t* counts, void* temp, size_t temp_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
  * Host-memory entry points: the drop-in path (H2D, sort, D2H inside).
  * ---------------------------------------------------------------------- */
 /* radix_sort_lsd(input, base): sort.hpp:40. */

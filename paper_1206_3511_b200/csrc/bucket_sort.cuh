@@ -499,3 +499,40 @@ __global__ void k_copy_range(const K* __restrict__ src, K* __restrict__ dst, con
 }
 
 }  // namespace isort
+
+namespace isort {
+
+// ------------------------------------------------------- key-range partition
+// Destination rank of a key for the multi-GPU sort: the number of splitters
+// <= key (splitters ascending), so rank r receives keys in [s_{r-1}, s_r).
+// One stable pass of the one-sweep pipeline with this digitizer partitions a
+// shard by destination while keeping input order inside each destination.
+constexpr int kMaxParts = 64;
+
+template <typename K>
+struct DestDigitizer {
+    static constexpr int kDigits = 1;
+    static constexpr bool kChecks = false;
+    static constexpr bool kCheapDigit = false;
+    K split[kMaxParts - 1];
+    int nsplit;
+    __device__ __forceinline__ uint32_t shift_for(int) const { return 0u; }
+    __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t) const {
+        uint32_t d = 0;
+#pragma unroll 8
+        for (int i = 0; i < kMaxParts - 1; ++i) {
+            if (i >= nsplit) break;
+            d += key >= split[i];
+        }
+        return d;
+    }
+    __device__ __forceinline__ uint32_t digit(K key, int) const { return digit_sh(key, 0u); }
+    __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const { d[0] = digit_sh(key, 0u); }
+    __device__ __forceinline__ bool in_range(K) const { return true; }
+};
+
+__global__ void k_copy_part_counts(const RadixState* __restrict__ st, uint64_t* __restrict__ counts, int parts) {
+    if (threadIdx.x < parts) counts[threadIdx.x] = st->hist[0][threadIdx.x];
+}
+
+}  // namespace isort

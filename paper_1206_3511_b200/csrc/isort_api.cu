@@ -528,6 +528,48 @@ int bucket_pairs_owned(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, ui
     return bucket_sort_device<K>(keys, keys_out, nullptr, idx, n, bound, ISORT_VALS_IOTA, temp.p, tb, s);
 }
 
+template <typename K>
+int partition_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, const K* splitters,
+                     int parts, int vmode, uint64_t* counts, void* temp, size_t temp_bytes, cudaStream_t s) {
+    if (parts < 1 || parts > kMaxParts)
+        return set_error(ISORT_EINVAL, "isort_partition: parts=%d outside [1, %d]", parts, kMaxParts);
+    if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
+        return set_error(ISORT_EINVAL, "isort_partition: bad vals_mode %d", vmode);
+    if (!counts) return set_error(ISORT_EINVAL, "isort_partition: null counts");
+    DestDigitizer<K> dz{};
+    dz.nsplit = parts - 1;
+    for (int i = 0; i + 1 < parts; ++i) {
+        dz.split[i] = splitters[i];
+        if (i && splitters[i] < splitters[i - 1]) return set_error(ISORT_EINVAL, "isort_partition: splitters not ascending");
+    }
+    if (n == 0) {
+        ISORT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * parts, s));
+        return ISORT_OK;
+    }
+    if (n > kMaxLookbackN)
+        return set_error(ISORT_ERANGE, "isort_partition: n=%llu exceeds the per-call limit", (unsigned long long)n);
+    const bool vals = vmode != ISORT_VALS_NONE;
+    if (!kin || !kout || (vals && !vout) || (vmode == ISORT_VALS_LOAD && !vin))
+        return set_error(ISORT_EINVAL, "isort_partition: null buffer");
+    const RadixLayout L = radix_layout<K>(n, vals);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.state);
+    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
+    auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
+    int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, vmode == ISORT_VALS_IOTA, n, st,
+                                                   lb, L.tiles, dz, true, true, s)
+                  : launch_radix_pipeline<K, false>(kin, kout, kalt, nullptr, nullptr, nullptr, false, n, st, lb,
+                                                    L.tiles, dz, true, true, s);
+    if (rc) return rc;
+    k_copy_part_counts<<<1, kMaxParts, 0, s>>>(st, counts, parts);
+    launched();
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
 }  // namespace isort
 
 using namespace isort;
@@ -619,6 +661,17 @@ int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uin
                           void* stream) {
     return bucket_sort_device<uint64_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
                                         temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t isort_partition_temp_bytes(uint64_t n, int key_bytes, int vals_mode) {
+    return isort_radix_temp_bytes(n, key_bytes, vals_mode);
+}
+
+int isort_partition_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                        uint64_t n, const uint32_t* splitters, int parts, int vals_mode, uint64_t* counts, void* temp,
+                        size_t temp_bytes, void* stream) {
+    return partition_device<uint32_t>(keys_in, keys_out, vals_in, vals_out, n, splitters, parts, vals_mode, counts,
+                                      temp, temp_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int isort_radix_sort_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t base, int device) {

@@ -1,0 +1,231 @@
+"""Multi-GPU sort by key-range partitioning.
+
+The reference is single-threaded and lists parallel sorting as future work
+(SPEC.md:8); this is the engine's scale-out step.  One process
+per GPU (torch.distributed, NCCL over NVLink/NVSwitch); rank r starts with the
+r-th positional shard of the input and ends with the r-th key range of the
+sorted output, so the global result is the rank-ordered concatenation:
+
+  1. sample      every rank takes S evenly spaced keys of its shard (device)
+  2. splitters   all_gather of the samples, device radix sort, the G-1 quantiles
+                 (key values: equal keys never straddle two ranks)
+  3. partition   one stable one-sweep pass with a destination-rank digitizer
+                 (isort_partition_u32): the shard grouped by destination, input
+                 order kept inside each group; per-destination counts
+  4. counts      all_gather of the G x G count matrix
+  5. exchange    all_to_all_single (NCCL grouped send/recv): chunks land ordered
+                 by source rank, i.e. in global input order
+  6. local sort  stable radix or bucket sort of the received keys
+
+Stability: received chunks are in source-rank (= input) order and the local
+sort is stable, so keys with equal value keep their global input order, and
+the concatenation over ranks equals the single-device stable sort bit for bit.
+
+Step 3 and 6 are CUDA kernels (via :class:`CudaOps`); steps 1-2 and 4-5 are
+collectives.  The protocol itself (:class:`KeyRangeSorter`) only talks to an
+ops object, which lets tests drive it over gloo on CPU with a torch-CPU stand-in
+for the kernels (tests/test_partition_gloo.py); the product path always uses
+CudaOps.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+
+DEFAULT_SAMPLE = 1 << 16
+
+
+@dataclass
+class PhaseTimes:
+    """Per-phase device times (ms) of one distributed sort on this rank."""
+
+    splitters: float = 0.0
+    partition: float = 0.0
+    exchange: float = 0.0
+    local_sort: float = 0.0
+    received: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class CudaOps:
+    """Kernels of the distributed sort on this rank's GPU (libisort.so)."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.lib = _lib.load()
+
+    def sample(self, keys: torch.Tensor, s: int) -> torch.Tensor:
+        n = keys.numel()
+        if n == 0:
+            return keys[:0].clone()
+        step = max(1, n // s)
+        return keys[::step][:s].contiguous()
+
+    def sort(self, keys: torch.Tensor) -> torch.Tensor:
+        from .device import radix_sort
+
+        k, _ = radix_sort(keys)
+        return k
+
+    def partition(self, keys, vals, splitters: list[int], parts: int):
+        n = keys.numel()
+        vmode = _lib.VALS_LOAD if vals is not None else _lib.VALS_NONE
+        out = torch.empty_like(keys)
+        vout = torch.empty_like(vals) if vals is not None else None
+        counts = torch.zeros(parts, dtype=torch.int64, device=self.device)
+        tb = self.lib.isort_partition_temp_bytes(n, 4, vmode)
+        temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
+        import ctypes
+
+        spl = (ctypes.c_uint32 * max(1, parts - 1))(*[int(x) & 0xFFFFFFFF for x in splitters])
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.isort_partition_u32(keys.data_ptr(), out.data_ptr(),
+                                                vals.data_ptr() if vals is not None else None,
+                                                vout.data_ptr() if vout is not None else None,
+                                                n, spl, parts, vmode, counts.data_ptr(), temp.data_ptr(), tb, s))
+        return out, vout, counts
+
+    def local_sort(self, keys, vals, algorithm: str, lo: int, hi: int):
+        from . import device
+
+        if keys.numel() == 0:
+            return keys, vals
+        if algorithm == "bucket":
+            k, v = device.bucket_sort(keys, hi, vals=vals)
+        else:
+            k, v = device.radix_sort(keys, vals=vals)
+        return k, v
+
+    def event(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    @staticmethod
+    def elapsed(a, b) -> float:
+        b.synchronize()
+        return a.elapsed_time(b)
+
+
+class KeyRangeSorter:
+    """Distributed stable sort of u32 keys (+ optional u32 payload) over a process group."""
+
+    def __init__(self, dist, ops, sample_per_rank: int = DEFAULT_SAMPLE, key_max: int = 0xFFFFFFFF):
+        self.dist = dist
+        self.ops = ops
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self.sample_per_rank = sample_per_rank
+        self.key_max = key_max
+
+    def splitters(self, keys: torch.Tensor) -> list[int]:
+        """G-1 ascending splitter key values from the gathered sample's quantiles."""
+        g = self.world
+        if g == 1:
+            return []
+        smp = self.ops.sample(keys, self.sample_per_rank)
+        sizes = torch.tensor([smp.numel()], dtype=torch.int64, device=smp.device)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(g)]
+        self.dist.all_gather(all_sizes, sizes)
+        sz = [int(x.item()) for x in all_sizes]
+        m = max(sz) if sz else 0
+        padded = torch.zeros(m, dtype=smp.dtype, device=smp.device)
+        padded[: smp.numel()] = smp
+        gathered = [torch.zeros_like(padded) for _ in range(g)]
+        self.dist.all_gather(gathered, padded)
+        pool = torch.cat([t[:s] for t, s in zip(gathered, sz)])
+        if pool.numel() == 0:
+            return [self.key_max] * (g - 1)
+        srt = self.ops.sort(pool)
+        # quantile i*len/g (as unsigned key values); equal keys never straddle ranks
+        idx = [min(srt.numel() - 1, (i * srt.numel()) // g) for i in range(1, g)]
+        vals = srt[torch.tensor(idx, device=srt.device)]
+        out = [int(v) & 0xFFFFFFFF for v in vals.tolist()]
+        for i in range(1, len(out)):  # ascending (duplicates allowed: empty ranges)
+            out[i] = max(out[i], out[i - 1])
+        return out
+
+    def sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None, algorithm: str = "radix"):
+        """Returns (this rank's sorted key range, payload or None, PhaseTimes)."""
+        g, me = self.world, self.rank
+        pt = PhaseTimes()
+        e0 = self.ops.event()
+        spl = self.splitters(keys)
+        e1 = self.ops.event()
+        if g > 1:
+            parted, pvals, counts = self.ops.partition(keys, vals, spl, g)
+        else:
+            parted, pvals, counts = keys, vals, None
+        e2 = self.ops.event()
+        if g > 1:
+            # count matrix: row = source rank, column = destination rank
+            allc = [torch.zeros_like(counts) for _ in range(g)]
+            self.dist.all_gather(allc, counts)
+            send = [int(x) for x in counts.tolist()]
+            recv = [int(allc[src][me].item()) for src in range(g)]
+            out = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
+            self.dist.all_to_all_single(out, parted, output_split_sizes=recv, input_split_sizes=send)
+            vout = None
+            if vals is not None:
+                vout = torch.empty(sum(recv), dtype=vals.dtype, device=vals.device)
+                self.dist.all_to_all_single(vout, pvals, output_split_sizes=recv, input_split_sizes=send)
+        else:
+            out, vout = parted, pvals
+        e3 = self.ops.event()
+        lo = spl[me - 1] if me > 0 else 0
+        hi = (spl[me] - 1) if me < g - 1 and spl[me] > 0 else self.key_max
+        hi = max(hi, lo)
+        sk, sv = self.ops.local_sort(out, vout, algorithm, lo, hi)
+        e4 = self.ops.event()
+        pt.splitters = self.ops.elapsed(e0, e1)
+        pt.partition = self.ops.elapsed(e1, e2)
+        pt.exchange = self.ops.elapsed(e2, e3)
+        pt.local_sort = self.ops.elapsed(e3, e4)
+        pt.received = int(out.numel())
+        return sk, sv, pt
+
+
+def bench_distributed(keys: torch.Tensor, algorithm: str, range_bound: int, steps: int, warmup: int, dist):
+    """Time `steps` distributed sorts of the per-rank shards (bench.py, N > 1).
+
+    Device time per step = max over ranks of (CUDA-event time from the first
+    barrier to the end of the local sort).  Returns (ms_per_step, info)."""
+    dev = keys.device
+    sorter = KeyRangeSorter(dist, CudaOps(dev))
+    l0 = _lib.load().isort_launch_count()
+    for _ in range(warmup):
+        sorter.sort(keys, algorithm=algorithm)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = []
+    l1 = _lib.load().isort_launch_count()
+    start.record()
+    for _ in range(steps):
+        _, _, pt = sorter.sort(keys, algorithm=algorithm)
+        phases.append(pt)
+    end.record()
+    torch.cuda.synchronize(dev)
+    launches = _lib.load().isort_launch_count() - l1
+    ms = torch.tensor([start.elapsed_time(end) / steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    avg = {k: sum(getattr(p, k) for p in phases) / len(phases)
+           for k in ("splitters", "partition", "exchange", "local_sort")}
+    recv = torch.tensor([float(phases[-1].received)], device=dev)
+    mx = recv.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    mean = recv.clone()
+    dist.all_reduce(mean, op=dist.ReduceOp.SUM)
+    info = {"phases": {k: round(v, 4) for k, v in avg.items()}, "launches": int(launches),
+            "max_over_mean_received": float(mx.item() / max(1.0, mean.item() / dist.get_world_size())),
+            "warmup_launches": int(l1 - l0)}
+    return float(ms.item()), info
+
+
+def _wallclock() -> float:  # pragma: no cover - helper for ad-hoc use
+    return time.perf_counter()

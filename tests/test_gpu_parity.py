@@ -16,7 +16,10 @@ from oracle.binding import RECORD_DTYPE
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 U32_MAX = (1 << 32) - 1
-TILE = 7680  # u32 keys-only / pairs one-sweep tile
+# one-sweep geometry: chunk = 512 threads x IPT keys, tile = 4 chunks
+# (keys-only IPT 12: 6144 / 24576; with payload IPT 8: 4096 / 16384)
+TILE = 24576
+BOUNDARIES = [4095, 4096, 4097, 6143, 6144, 6145, 16383, 16384, 16385, 24575, 24576, 24577, 2 * 24576 + 17]
 
 
 def recs(keys):
@@ -93,7 +96,7 @@ def test_device_bucket_index_matches_reference(cuda, golden):
 
 
 # ------------------------------------------------------- device API vs oracle
-SIZES = [1, 2, 31, 32, 33, 1000, TILE - 1, TILE, TILE + 1, 2 * TILE + 17, 100_000, 1_000_003]
+SIZES = [1, 2, 31, 32, 33, 1000, *BOUNDARIES, 100_000, 1_000_003]
 
 
 def _dist(name, n, rng):
@@ -246,3 +249,49 @@ def test_full_size_radix_and_bucket_10e8(cuda, oracle):
         assert np.array_equal(got_i, want_i), alg
         got_k, _ = dev_sort(k, alg, None, range_bound=U32_MAX)
         assert np.array_equal(got_k, want_k), alg
+
+
+# ------------------------------------------------------- key-range partition kernel (multi-GPU step 3)
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_partition_kernel_is_stable_grouping(cuda, parts):
+    import torch
+
+    from paper_1206_3511_b200.partition import CudaOps
+
+    rng = np.random.default_rng(parts)
+    ops = CudaOps(torch.device("cuda:0"))
+    for n in (1, 1000, TILE * 5 + 3, 3_000_000):
+        k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        spl = sorted(int(x) for x in rng.integers(0, 1 << 32, size=parts - 1, dtype=np.uint64))
+        v = np.arange(n, dtype=np.int32)
+        tk = torch.from_numpy(k.view(np.int32)).cuda()
+        tv = torch.from_numpy(v).cuda()
+        ok, ov, cnt = ops.partition(tk, tv, spl, parts)
+        dest = np.searchsorted(np.array(spl, dtype=np.uint64), k.astype(np.uint64), side="right")
+        order = np.argsort(dest, kind="stable")
+        assert np.array_equal(cnt.cpu().numpy(), np.bincount(dest, minlength=parts)), (parts, n)
+        assert np.array_equal(ok.cpu().numpy().view(np.uint32), k[order]), (parts, n)
+        assert np.array_equal(ov.cpu().numpy(), v[order]), (parts, n)
+
+
+def test_key_range_protocol_single_rank_gpu(cuda, oracle):
+    """World size 1 through the same protocol object (no exchange), GPU kernels."""
+    import torch
+
+    from paper_1206_3511_b200.partition import CudaOps, KeyRangeSorter
+
+    class OneRank:
+        def get_world_size(self):
+            return 1
+
+        def get_rank(self):
+            return 0
+
+    k = oracle.mixture_u32(2_000_000, 7)
+    want_k, want_i = oracle.sort_u32(k, with_index=True)
+    tk = torch.from_numpy(k.view(np.int32)).cuda()
+    tv = torch.arange(k.size, dtype=torch.int32, device="cuda")
+    for alg in ("radix", "bucket"):
+        sk, sv, _ = KeyRangeSorter(OneRank(), CudaOps(torch.device("cuda:0"))).sort(tk, tv, algorithm=alg)
+        assert np.array_equal(sk.cpu().numpy().view(np.uint32), want_k)
+        assert np.array_equal(sv.cpu().numpy().view(np.uint32), want_i)
