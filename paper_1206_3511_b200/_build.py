@@ -64,9 +64,20 @@ def build_oracle(verbose: bool = False) -> None:
                    stdout=None if verbose else subprocess.DEVNULL)
 
 
+def build_dropin(verbose: bool = False) -> None:
+    """The C++ drop-in (dropin/sort_b200.cpp) linked with the reference's other
+    sources and its own test suites -- only where /root/reference exists; the
+    binaries travel to the GPU box prebuilt under oracle/_ref/."""
+    if not os.path.isdir(REFERENCE):
+        return
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin"], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_engine(force=force, verbose=verbose)
     build_oracle(verbose=verbose)
+    build_dropin(verbose=verbose)
 
 
 if __name__ == "__main__":
