@@ -84,7 +84,7 @@ struct PassCfg {
     static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : 12) : (VALS ? 6 : 8);
     static constexpr int kChunks = 4;
     static constexpr int kTile = kBlock * kIpt * kChunks;
-    static constexpr int kCtasPerSm = 2048 / kBlock;
+    static constexpr int kCtasPerSm = 1024 / kBlock;
 };
 
 // Upfront histogram replication (lane copies per bin): 64 KB of counters.

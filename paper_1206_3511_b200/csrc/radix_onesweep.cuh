@@ -389,7 +389,7 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE>
-__global__ void __launch_bounds__(BLOCK, 2048 / BLOCK)
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,

@@ -37,17 +37,30 @@ h = src[1]
 ix = {k: i for i, k in enumerate(h)}
 data = src[2:]
 S = "Warp Stall Sampling (All Samples)"
-tot = sum(float(r[ix[S]] or 0) for r in data) or 1
+
+
+def num(x):
+    try:
+        return float(str(x).replace(",", ""))
+    except ValueError:
+        return 0.0
+
+
+data = [r for r in data if len(r) == len(h) and r[ix["Source"]] != "Source"]
+for r in data:
+    r[ix[S]] = num(r[ix[S]])
+    r[ix["Instructions Executed"]] = num(r[ix["Instructions Executed"]])
+tot = sum(r[ix[S]] for r in data) or 1
 print("top stall sites:")
-for r in sorted(data, key=lambda r: -float(r[ix[S]] or 0))[:top]:
-    print(f"  {float(r[ix[S]]) / tot * 100:5.1f}%  {r[ix['Source']][:70]:70} exec={r[ix['Instructions Executed']]}")
+for r in sorted(data, key=lambda r: -r[ix[S]])[:top]:
+    print(f"  {r[ix[S]] / tot * 100:5.1f}%  {r[ix['Source']][:70]:70} exec={r[ix['Instructions Executed']]:.0f}")
 c = collections.Counter()
 for r in data:
     op = r[ix["Source"]].split()
     if not op:
         continue
     o = op[1] if op[0].startswith("@") else op[0]
-    c[o.split(".")[0]] += float(r[ix["Instructions Executed"]] or 0)
+    c[o.split(".")[0]] += r[ix["Instructions Executed"]]
 t = sum(c.values())
 print("instruction mix (warp-level):", f"{t / 1e6:.1f}M total")
 print("  " + ", ".join(f"{k} {v / t * 100:.1f}%" for k, v in c.most_common(16)))
