@@ -126,10 +126,40 @@ struct BucketIndexer {
     }
 };
 
-constexpr int kBucketMaxDigits = 3;
-constexpr uint32_t kSuperBucketBits = 11;  // super-bucket = up to 2^11 buckets
+// Divisor kinds, chosen on the host once per call (compile-time in the kernels):
+//   kPow2Narrow   count * key < 2^64 and M + 1 = 2^s: one 64-bit multiply and a shift
+//   kMagicNarrow  count * key < 2^64: 64-bit magic reciprocal + <= 2 corrections
+//   kWide         general 128-by-64 division (BucketIndexer::bucket)
+enum BucketMode : int { kPow2Narrow = 0, kMagicNarrow = 1, kWide = 2 };
 
-template <typename K>
+template <int MODE>
+__device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t key) {
+    if (MODE == kWide) return bi.bucket(key);
+    if (key > bi.bound) return bi.count - 1;
+    const uint64_t p = bi.count * key;  // exact: narrow modes guarantee < 2^64
+    if (MODE == kPow2Narrow) return bi.pow2_shift >= 64 ? 0ull : p >> bi.pow2_shift;
+    uint64_t q = __umul64hi(p, bi.magic);
+    uint64_t r = p - q * bi.div;
+    if (r >= bi.div) {
+        ++q;
+        r -= bi.div;
+    }
+    if (r >= bi.div) ++q;
+    return q;
+}
+
+inline int choose_bucket_mode(uint64_t count, uint64_t bound, uint64_t key_max) {
+    const uint64_t kmax = bound < key_max ? bound : key_max;
+    const bool narrow = static_cast<unsigned __int128>(count) * kmax < (static_cast<unsigned __int128>(1) << 64);
+    if (!narrow) return kWide;
+    const bool pow2 = bound == ~0ull || ((bound + 1) & bound) == 0;
+    return pow2 ? kPow2Narrow : kMagicNarrow;
+}
+
+constexpr int kBucketMaxDigits = 3;
+constexpr uint32_t kSuperBucketBits = 11;  // super-bucket = up to 2^11 consecutive buckets
+
+template <typename K, int MODE = kWide>
 struct BucketDigitizer {
     static constexpr int kDigits = kBucketMaxDigits;
     static constexpr bool kChecks = true;
@@ -157,17 +187,18 @@ struct BucketDigitizer {
         return pos == 0 ? shift[0] : (pos == 1 ? shift[1] : shift[2]);
     }
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
-        return static_cast<uint32_t>(bi.bucket(static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
+        return static_cast<uint32_t>(bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
     }
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
-        const uint64_t b = bi.bucket(static_cast<uint64_t>(key));
+        const uint64_t b = bucket_of<MODE>(bi, static_cast<uint64_t>(key));
 #pragma unroll
         for (int p = 0; p < kDigits; ++p) d[p] = static_cast<uint32_t>(b >> shift[p]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const { return static_cast<uint64_t>(key) <= bi.bound; }
+    __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }
     __device__ __forceinline__ uint64_t super_bucket(K key) const {
-        return bi.bucket(static_cast<uint64_t>(key)) >> s_lo;
+        return bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> s_lo;
     }
 };
 
@@ -196,13 +227,14 @@ struct WindowSummary {  // per window: first super-bucket start, min/max of the 
 template <int BLOCK, int IPT>
 struct WindowCfg {
     static constexpr int kStage = BLOCK * IPT;  // keys staged per CTA
-    static constexpr int kWindow = kStage / 2;  // owned range
+    static constexpr int kWindow = kStage / 2;  // owned range; reach = 1 window (super-buckets ~2K keys)
     static constexpr int kCap = kStage - kWindow;  // reach past the window
     static constexpr int kWarps = BLOCK / 32;
 };
 
 constexpr int kWinDigitBits = 9;  // window sort digit width (<= 9 bits: 512 bins)
 constexpr int kWinBins = 1 << kWinDigitBits;
+static_assert(kWinBins % 256 == 0 || kWinBins <= 256, "bins split evenly over the window CTA");
 
 template <typename K, int BLOCK, int IPT, bool VALS>
 struct WindowSmem {
@@ -213,6 +245,8 @@ struct WindowSmem {
     uint32_t cnt[BLOCK / 32][kWinBins];  // per-warp digit counters, then slot bases
     uint32_t scan_tot[BLOCK / 32];
     unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32];
+    unsigned long long red6[6][BLOCK / 32];
+    uint32_t prev_sb;
     int first, last, end;
 };
 
@@ -274,7 +308,7 @@ __device__ __forceinline__ int warp_lower_bound(int lo, int hi, Pred pred) {
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, bool VALS>
-__global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_bucket_windows(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
                                                           const RadixState* __restrict__ rst,
                                                           BucketState* __restrict__ bst,
                                                           WindowSummary<K>* __restrict__ summ,
@@ -292,94 +326,165 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
     const int avail = static_cast<int>((n - w0 < static_cast<uint64_t>(kStage) ? n - w0 : static_cast<uint64_t>(kStage)));
     const int wlen = min(kWindow, avail);
 
-    for (int j = tid; j < avail; j += BLOCK) {
-        sm.keys[j] = keys[w0 + j];
-        if (VALS) sm.vals[j] = vals[w0 + j];
+#ifdef ISORT_PHASE_TIMING
+    long long t0 = clock64(), t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    unsigned long long* prof = const_cast<unsigned long long*>(rst->prof);
+#define WTICK(v) v = clock64()
+#define WFLUSH(k)                                                                      \
+    if (tid == 0) {                                                                    \
+        const long long tn = clock64();                                                \
+        atomicAdd(prof + 8, (unsigned long long)((t1 ? t1 : tn) - t0));               \
+        if (t1) atomicAdd(prof + 9, (unsigned long long)((t2 ? t2 : tn) - t1));       \
+        if (t2) atomicAdd(prof + 10, (unsigned long long)((t3 ? t3 : tn) - t2));      \
+        if (t3) atomicAdd(prof + 11, (unsigned long long)((t4 ? t4 : tn) - t3));      \
+        if (t4) atomicAdd(prof + 12, (unsigned long long)(tn - t4));                  \
+        atomicAdd(prof + 13 + (k), 1ull);                                              \
     }
-    __syncthreads();
-    // The passes left the array ordered by super-bucket, so the super-bucket id is
-    // non-decreasing in position and every boundary is a binary search (warp 0).
-    if (warp == 0) {
-        auto sb_at = [&](int j) { return dz.super_bucket(sm.keys[j]); };
-        int first = 0;
-        if (w0 != 0) {
-            const uint64_t prev = dz.super_bucket(keys[w0 - 1]);
-            first = warp_lower_bound(0, wlen, [&](int j) { return sb_at(j) > prev; });
-        }
-        int last = wlen, end = avail;
-        if (first < wlen) {
-            const uint64_t tail = sb_at(wlen - 1);
-            last = warp_lower_bound(first, wlen - 1, [&](int j) { return sb_at(j) >= tail; });
-            end = warp_lower_bound(wlen, avail, [&](int j) { return sb_at(j) > tail; });
-        }
-        if (lane == 0) {
-            sm.first = first;
-            sm.last = last;
-            sm.end = end;
-        }
-    }
-    __syncthreads();
-    const int first = sm.first;
-    int end = sm.end;
-
-    // summary for K6: keys before the first owned super-bucket (they belong to an earlier one)
+#else
+#define WTICK(v)
+#define WFLUSH(k)
+#endif
+    // ---- stage [w0, w0 + avail); super-bucket id (low 32 bits: adjacent ids differ
+    // by far less than 2^32, so equality is exact) kept per position in sm.keys2
+    uint32_t* sbuf = reinterpret_cast<uint32_t*>(sm.keys2);
     {
-        K hmin = static_cast<K>(~static_cast<K>(0)), hmax = 0;
-        for (int j = tid; j < first; j += BLOCK) {
-            const K k = sm.keys[j];
-            hmin = k < hmin ? k : hmin;
-            hmax = k > hmax ? k : hmax;
+        K stage[IPT];
+        uint32_t vstage[VALS ? IPT : 1];
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int j = tid + i * BLOCK;
+            if (j < avail) {
+                stage[i] = keys[w0 + j];
+                if (VALS) vstage[i] = vals[w0 + j];
+            }
         }
-        unsigned long long a, b;
-        block_minmax(hmin, hmax, sm.red_a, sm.red_b, kWarps, a, b);
-        if (tid == 0) {
-            summ[blockIdx.x].first = first < wlen ? w0 + first : ~0ull;
-            summ[blockIdx.x].hmin = a;
-            summ[blockIdx.x].hmax = b;
+        if (tid == 0) sm.prev_sb = w0 ? static_cast<uint32_t>(dz.super_bucket(keys[w0 - 1])) : 0u;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int j = tid + i * BLOCK;
+            if (j < avail) {
+                sm.keys[j] = stage[i];
+                sbuf[j] = static_cast<uint32_t>(dz.super_bucket(stage[i]));
+                if (VALS) sm.vals[j] = vstage[i];
+            }
         }
     }
-    if (first >= wlen) return;  // no super-bucket starts here
-
-    if (end == avail && w0 + avail < n) {
-        // The last owned super-bucket runs past the staged range: oversized.
-        // Record it (K6 resolves its end and whether it is constant); sort the rest.
-        const int ostart = sm.last;
-        K omin = static_cast<K>(~static_cast<K>(0)), omax = 0;
-        for (int j = ostart + tid; j < avail; j += BLOCK) {
-            const K k = sm.keys[j];
-            omin = k < omin ? k : omin;
-            omax = k > omax ? k : omax;
+    __syncthreads();
+    WTICK(t1);
+    // ---- super-bucket starts (all threads): first/last start in [0, wlen), first start in [wlen, avail)
+    {
+        int my_first = 0x7fffffff, my_last = -1, my_end = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int j = tid + i * BLOCK;
+            if (j < avail) {
+                const bool start = (w0 + j == 0) || sbuf[j] != (j ? sbuf[j - 1] : sm.prev_sb);
+                if (start) {
+                    if (j < wlen) {
+                        my_first = min(my_first, j);
+                        my_last = max(my_last, j);
+                    } else {
+                        my_end = min(my_end, j);
+                    }
+                }
+            }
         }
-        unsigned long long a, b;
-        block_minmax(omin, omax, sm.red_a, sm.red_b, kWarps, a, b);
+        my_first = __reduce_min_sync(ISORT_FULL_MASK, my_first);
+        my_last = __reduce_max_sync(ISORT_FULL_MASK, my_last);
+        my_end = __reduce_min_sync(ISORT_FULL_MASK, my_end);
         if (tid == 0) {
+            sm.first = 0x7fffffff;
+            sm.last = -1;
+            sm.end = 0x7fffffff;
+        }
+        __syncthreads();
+        if (lane == 0) {
+            if (my_first != 0x7fffffff) atomicMin(&sm.first, my_first);
+            if (my_last >= 0) atomicMax(&sm.last, my_last);
+            if (my_end != 0x7fffffff) atomicMin(&sm.end, my_end);
+        }
+        __syncthreads();
+    }
+    WTICK(t2);
+    const int first = min(sm.first, wlen);
+    int end = min(sm.end, avail);
+    const bool oversized = first < wlen && end == avail && w0 + avail < n;
+    const int ostart = sm.last;
+    if (oversized) end = ostart;  // the trailing super-bucket is resolved by K6
+    // ---- one block reduction: head (before `first`), sort range, oversized tail
+    K hmin = static_cast<K>(~static_cast<K>(0)), hmax = 0, rmin = hmin, rmax = 0, omin = hmin, omax = 0;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int j = tid + i * BLOCK;
+        if (j < avail) {
+            const K k = sm.keys[j];
+            if (j < first) {
+                hmin = k < hmin ? k : hmin;
+                hmax = k > hmax ? k : hmax;
+            } else if (j < end) {
+                rmin = k < rmin ? k : rmin;
+                rmax = k > rmax ? k : rmax;
+            } else if (oversized) {
+                omin = k < omin ? k : omin;
+                omax = k > omax ? k : omax;
+            }
+        }
+    }
+    {
+        unsigned long long v[6] = {~static_cast<unsigned long long>(hmin), hmax, ~static_cast<unsigned long long>(rmin),
+                                   rmax, ~static_cast<unsigned long long>(omin), omax};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = warp_max<unsigned long long>(v[q]);
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) sm.red6[q][warp] = v[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            unsigned long long x = 0;
+            for (int w = 0; w < kWarps; ++w) x = sm.red6[q][w] > x ? sm.red6[q][w] : x;
+            v[q] = x;
+        }
+        hmin = static_cast<K>(~v[0]);
+        hmax = static_cast<K>(v[1]);
+        rmin = static_cast<K>(~v[2]);
+        rmax = static_cast<K>(v[3]);
+        omin = static_cast<K>(~v[4]);
+        omax = static_cast<K>(v[5]);
+    }
+    if (tid == 0) {
+        summ[blockIdx.x].first = first < wlen ? w0 + first : ~0ull;
+        summ[blockIdx.x].hmin = first > 0 ? static_cast<unsigned long long>(hmin) : ~0ull;
+        summ[blockIdx.x].hmax = first > 0 ? static_cast<unsigned long long>(hmax) : 0ull;
+        if (oversized) {
             const uint32_t r = atomicAdd(&bst->n_over, 1u);
             over[r].start = w0 + ostart;
-            over[r].kmin = a;
-            over[r].kmax = b;
+            over[r].kmin = omin;
+            over[r].kmax = omax;
             over[r].window = blockIdx.x;
         }
-        end = ostart;
+    }
+    WTICK(t3);
+    if (first >= wlen) {  // no super-bucket starts here
+        WFLUSH(0);
+        return;
     }
     const int len = end - first;
-    if (len <= 1) return;
+    if (len <= 1) {
+        WFLUSH(1);
+        return;
+    }
 
     // ---- stable in-smem LSD sort of sm.keys[first, end) by (key - min), r-bit digits
     // Same rank primitive as the one-sweep pass: per-warp counters pre-scanned into
     // slot bases, slot = atomicAdd (lane-ordered, program-ordered => stable).
-    K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
-    for (int j = first + tid; j < end; j += BLOCK) {
-        const K k = sm.keys[j];
-        kmin = k < kmin ? k : kmin;
-        kmax = k > kmax ? k : kmax;
+    const K kmin = rmin, kmax = rmax;
+    WTICK(t4);
+    if (kmin == kmax) {  // one key value: arrival order is the answer
+        WFLUSH(1);
+        return;
     }
-    {
-        unsigned long long a, b;
-        block_minmax(kmin, kmax, sm.red_a, sm.red_b, kWarps, a, b);
-        kmin = static_cast<K>(a);
-        kmax = static_cast<K>(b);
-    }
-    if (kmin == kmax) return;  // one key value: arrival order is the answer
     const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
     const int passes = (bits + kWinDigitBits - 1) / kWinDigitBits;
     const int r = (bits + passes - 1) / passes;
@@ -388,43 +493,62 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
     K* kb = sm.keys2;
     uint32_t* va = sm.vals + first;
     uint32_t* vb = sm.vals2;
-    const int wofs = warp * 32 * IPT + static_cast<int>(lane);
+    // items per thread sized to this window's range, so every warp has work
+    const int ipt = (len + BLOCK - 1) / BLOCK;
+    const int wofs = warp * 32 * ipt + static_cast<int>(lane);
     for (int pass = 0; pass < passes; ++pass) {
         const uint32_t shift = static_cast<uint32_t>(pass * r);
-        for (int i = tid; i < kWarps * kWinBins; i += BLOCK) (&sm.cnt[0][0])[i] = 0;
+        for (int i = tid; i < kWarps * static_cast<int>(nbins); i += BLOCK)
+            sm.cnt[i / static_cast<int>(nbins)][i % static_cast<int>(nbins)] = 0;
         __syncthreads();
         uint32_t* wc = sm.cnt[warp];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int o = wofs + i * 32;
-            if (o < len) atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
+            if (i < ipt && o < len)
+                atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
         }
         __syncthreads();
-        // bin b (one per thread): totals over warps, block scan over bins, per-warp bases
-        uint32_t tot = 0;
-        const uint32_t b = static_cast<uint32_t>(tid);
-        if (b < nbins) {
+        // bins [tid*BPT, tid*BPT + BPT): totals over warps, block scan over bins, per-warp bases
+        constexpr int BPT = kWinBins / BLOCK > 0 ? kWinBins / BLOCK : 1;
+        uint32_t btot[BPT], tsum = 0;
+#pragma unroll
+        for (int q = 0; q < BPT; ++q) {
+            const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
+            uint32_t t = 0;
+            if (b < nbins) {
 #pragma unroll 4
-            for (int w = 0; w < kWarps; ++w) tot += sm.cnt[w][b];
+                for (int w = 0; w < kWarps; ++w) t += sm.cnt[w][b];
+            }
+            btot[q] = t;
+            tsum += t;
         }
-        const uint32_t inc = warp_inclusive_scan(tot);
+        const uint32_t inc = warp_inclusive_scan(tsum);
         if (lane == 31) sm.scan_tot[warp] = inc;
         __syncthreads();
-        if (b < nbins) {
-            uint32_t base = inc - tot;
+        {
+            uint32_t base = inc - tsum;
             for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
+#pragma unroll
+            for (int q = 0; q < BPT; ++q) {
+                const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
+                if (b < nbins) {
+                    uint32_t bb = base;
 #pragma unroll 4
-            for (int w = 0; w < kWarps; ++w) {
-                const uint32_t v = sm.cnt[w][b];
-                sm.cnt[w][b] = base;
-                base += v;
+                    for (int w = 0; w < kWarps; ++w) {
+                        const uint32_t v = sm.cnt[w][b];
+                        sm.cnt[w][b] = bb;
+                        bb += v;
+                    }
+                }
+                base += btot[q];
             }
         }
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int o = wofs + i * 32;
-            if (o < len) {
+            if (i < ipt && o < len) {
                 const K k = ka[o];
                 const uint32_t slot = atomicAdd(&wc[static_cast<uint32_t>((k - kmin) >> shift) & mask], 1u);
                 kb[slot] = k;
@@ -443,6 +567,9 @@ __global__ void __launch_bounds__(BLOCK) k_bucket_windows(K* __restrict__ keys, 
         keys[w0 + first + j] = ka[j];
         if (VALS) vals[w0 + first + j] = va[j];
     }
+    WFLUSH(2);
+#undef WTICK
+#undef WFLUSH
 }
 
 // ------------------------------------------------------------------ K6

@@ -433,9 +433,26 @@ BucketLayout bucket_layout(uint64_t n, bool vals) {
     return L;
 }
 
+template <typename K, int MODE>
+int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s);
+
 template <typename K>
 int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
                        int vmode, void* temp, size_t temp_bytes, cudaStream_t s) {
+    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)))) {
+        case kPow2Narrow:
+            return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
+        case kMagicNarrow:
+            return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
+        default:
+            return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
+    }
+}
+
+template <typename K, int MODE>
+int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s) {
     static_assert(KeyTraits<K>::kDigits >= kBucketMaxDigits, "look-back sized for the bucket digit slots");
     g_last_bad_index = ~0ull;
     if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
@@ -458,7 +475,7 @@ int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vou
     auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
     auto* summ = reinterpret_cast<WindowSummary<K>*>(t + L.summ);
     auto* over = reinterpret_cast<OverRec*>(t + L.over);
-    const BucketDigitizer<K> dz = BucketDigitizer<K>::make(n, bound);
+    const BucketDigitizer<K, MODE> dz = BucketDigitizer<K, MODE>::make(n, bound);
     const bool iota = vmode == ISORT_VALS_IOTA;
 
     int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, iota, n, st, lb, L.r.tiles, dz,
@@ -469,12 +486,12 @@ int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vou
     ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
     if (vals) {
         using Smem = WindowSmem<K, kWinBlock, kWinIpt, true>;
-        auto* kern = k_bucket_windows<K, BucketDigitizer<K>, kWinBlock, kWinIpt, true>;
+        auto* kern = k_bucket_windows<K, BucketDigitizer<K, MODE>, kWinBlock, kWinIpt, true>;
         set_max_smem_once(kern, sizeof(Smem));
         kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, vout, n, st, bst, summ, over, dz);
     } else {
         using Smem = WindowSmem<K, kWinBlock, kWinIpt, false>;
-        auto* kern = k_bucket_windows<K, BucketDigitizer<K>, kWinBlock, kWinIpt, false>;
+        auto* kern = k_bucket_windows<K, BucketDigitizer<K, MODE>, kWinBlock, kWinIpt, false>;
         set_max_smem_once(kern, sizeof(Smem));
         kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, nullptr, n, st, bst, summ, over, dz);
     }
