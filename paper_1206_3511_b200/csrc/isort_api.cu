@@ -75,17 +75,27 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 
 // ----------------------------------------------------- kernel configuration
 // Tile shapes per (key width, payload).  Tile = BLOCK * IPT keys.
-template <typename K, bool VALS>
-struct PassCfg {
 #ifndef ISORT_PASS_BLOCK
 #define ISORT_PASS_BLOCK 512
 #endif
+// One-sweep tile shape: BLOCK threads x IPT keys per chunk, CHUNKS chunks per
+// tile.  Large inputs use 4-chunk tiles (short look-back walks); inputs below
+// kSmallN use 1-chunk tiles so a few million keys still fill all SMs.
+constexpr uint64_t kSmallN = 4ull << 20;
+
+template <typename K, bool VALS, int CHUNKS = 4>
+struct PassCfg {
     static constexpr int kBlock = ISORT_PASS_BLOCK;
     static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : 12) : (VALS ? 6 : 8);
-    static constexpr int kChunks = 4;
+    static constexpr int kChunks = CHUNKS;
     static constexpr int kTile = kBlock * kIpt * kChunks;
     static constexpr int kCtasPerSm = 1024 / kBlock;
 };
+
+template <typename K, bool VALS>
+inline int pass_tile(uint64_t n) {
+    return n < kSmallN ? PassCfg<K, VALS, 1>::kTile : PassCfg<K, VALS, 4>::kTile;
+}
 
 // Upfront histogram replication (lane copies per bin): 64 KB of counters.
 template <int D>
@@ -133,13 +143,19 @@ struct RadixLayout {
 template <typename K>
 RadixLayout radix_layout(uint64_t n, bool vals) {
     RadixLayout L;
-    const int tile = vals ? PassCfg<K, true>::kTile : PassCfg<K, false>::kTile;
+    const int tile = vals ? pass_tile<K, true>(n) : pass_tile<K, false>(n);
     L.tiles = static_cast<uint32_t>((n + tile - 1) / tile);
+    // Look-back rows for the worst tile count of any span m <= n (the bucket
+    // sort's oversized fallback sorts a sub-span with the small-n tile).
+    const uint64_t small = n < kSmallN ? n : kSmallN - 1;
+    const int stile = vals ? pass_tile<K, true>(small) : pass_tile<K, false>(small);
+    const uint64_t stiles = (small + stile - 1) / stile;
+    const uint64_t lb_tiles = stiles > L.tiles ? stiles : L.tiles;
     size_t off = 0;
     L.state = off;
     off += align_up(sizeof(RadixState));
     L.lookback = off;
-    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * L.tiles * kRadix * sizeof(uint32_t));
+    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * sizeof(uint32_t));
     L.keys_alt = off;
     off += align_up(n * sizeof(K));
     L.vals_alt = off;
@@ -164,6 +180,25 @@ void set_max_smem_once(F* kernel, size_t bytes) {
     g_smem_done.insert(key);
 }
 
+template <typename K, bool VALS, typename Dz, typename Cfg>
+void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
+                   uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s) {
+    constexpr int D = Dz::kDigits;
+    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
+    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false>
+                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true>;
+    set_max_smem_once(kern, sizeof(Smem));
+    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * kNumSMs) ? tiles
+                                                                                     : Cfg::kCtasPerSm * kNumSMs;
+    for (int slot = 0; slot < D; ++slot) {
+        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
+                                                        tiles, slot, dz);
+        static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
+                                                     "pass4", "pass5", "pass6", "pass7"};
+        prof_mark(s, kPassNames[slot]);
+    }
+}
+
 // Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
 // bucket sort's bucket-index digits).  Buffers: kin (const) -> kout, with kalt
 // as ping-pong; the plan decides which passes run.
@@ -172,7 +207,6 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
                           uint32_t* valt, bool iota, uint64_t n, RadixState* st, uint32_t* lookback,
                           uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
                           cudaStream_t s) {
-    using Cfg = PassCfg<K, VALS>;
     constexpr int D = Dz::kDigits;
     prof_mark(s, "start");
     g_prof.st = st;
@@ -200,22 +234,15 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     prof_mark(s, "plan");
     launched(2);
 
-    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
-    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false>
-                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true>;
-    set_max_smem_once(kern, sizeof(Smem));
-    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * kNumSMs) ? tiles
-                                                                                     : Cfg::kCtasPerSm * kNumSMs;
-    for (int slot = 0; slot < D; ++slot) {
-        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st,
-                                                        lookback, tiles, slot, dz);
-        static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
-                                                     "pass4", "pass5", "pass6", "pass7"};
-        prof_mark(s, kPassNames[slot]);
-    }
-    launched(D + 1);
-    const uint64_t cblocks = (n + 1023) / 1024;
-    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 8ull * kNumSMs ? cblocks : 8ull * kNumSMs), 256, 0, s>>>(
+    if (n < kSmallN)
+        launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
+                                                        dz, s);
+    else
+        launch_passes<K, VALS, Dz, PassCfg<K, VALS, 4>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
+                                                        dz, s);
+    launched(D);
+    const uint64_t cblocks = (n + 4095) / 4096;
+    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 4ull * kNumSMs ? (cblocks ? cblocks : 1) : 4ull * kNumSMs), 512, 0, s>>>(
         kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
     prof_mark(s, "copy");
     ISORT_CUDA_TRY(cudaGetLastError());

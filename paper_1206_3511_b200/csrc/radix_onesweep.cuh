@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     constexpr int kChunk = Smem::kChunk;
     constexpr int kTile = Smem::kTile;
     static_assert(BLOCK % kRadix == 0, "threads [0, kRadix) own one digit each in the per-tile section");
-    static_assert(NCHUNK % 2 == 0, "phase-1 loads are batched two chunks at a time");
+    static_assert(NCHUNK % 2 == 0 || NCHUNK == 1, "phase-1 loads are batched two chunks at a time");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -448,16 +448,35 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 
         // ---------------- phase 1: per-(chunk, warp) digit counts
 #pragma unroll 1
-        for (int c = 0; c < NCHUNK; c += 2) {
+        for (int c = 0; c < NCHUNK; c += (NCHUNK >= 2 ? 2 : 1)) {
             const uint32_t c0 = static_cast<uint32_t>(c) * kChunk + static_cast<uint32_t>(warp) * 32u * IPT;
             const uint32_t c1 = c0 + kChunk;
             uint32_t* wc0 = sm.cnt[c][warp];
-            uint32_t* wc1 = sm.cnt[c + 1][warp];
+            uint32_t* wc1 = sm.cnt[NCHUNK >= 2 ? c + 1 : c][warp];
             const K* ws = src + tile_base + c0;
+            if (NCHUNK == 1) {
+                if (vec && c0 + 32u * IPT <= tile_len) {
+                    const uint4* v0 = reinterpret_cast<const uint4*>(ws);
+                    uint4 x[IPT / 4 > 0 ? IPT / 4 : 1];
+#pragma unroll
+                    for (int q = 0; q < IPT / 4; ++q) x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
+#pragma unroll
+                    for (int q = 0; q < IPT / 4; ++q) {
+                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].x), dsh)], 1u);
+                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].y), dsh)], 1u);
+                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].z), dsh)], 1u);
+                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].w), dsh)], 1u);
+                    }
+                } else {
+                    for (uint32_t o = lane; o < 32u * IPT; o += 32)
+                        if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
+                }
+                continue;
+            }
             if (vec && c1 + 32u * IPT <= tile_len) {
                 const uint4* v0 = reinterpret_cast<const uint4*>(ws);
                 const uint4* v1 = reinterpret_cast<const uint4*>(ws + kChunk);
-                uint4 x[IPT / 4], y[IPT / 4];
+                uint4 x[IPT / 4 > 0 ? IPT / 4 : 1], y[IPT / 4 > 0 ? IPT / 4 : 1];
 #pragma unroll
                 for (int q = 0; q < IPT / 4; ++q) {
                     x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
@@ -595,9 +614,20 @@ __global__ void k_copy_if_unsorted_skip(const K* __restrict__ in, K* __restrict_
                                         int iota_vals, uint64_t n, const RadixState* __restrict__ st) {
     if (!st->copy_in_to_out) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        out[i] = in[i];
-        if (vout) vout[i] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // 16-byte vectors when both pointers are aligned (the common case), scalar tail
+    constexpr uint64_t kPer = 16 / sizeof(K);
+    uint64_t done = 0;
+    if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) {
+        const uint64_t nv = n / kPer;
+        const uint4* s4 = reinterpret_cast<const uint4*>(in);
+        uint4* d4 = reinterpret_cast<uint4*>(out);
+        for (uint64_t v = t0; v < nv; v += stride) d4[v] = ldg_stream_v4(s4 + v);
+        done = nv * kPer;
+    }
+    for (uint64_t i = done + t0; i < n; i += stride) out[i] = in[i];
+    if (vout) {
+        for (uint64_t i = t0; i < n; i += stride) vout[i] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
     }
 }
 
