@@ -16,16 +16,16 @@
 //       8*D_b bits of b), bucket order, arrival order kept.    D_b x 8n B
 //       D_b = ceil((L - 11) / 8) for L = bits(n - 1): a super-bucket covers
 //       <= 2^11 buckets (~2K keys on average).
-//   K5  k_bucket_windows: each CTA owns the super-buckets that START in its
-//       window, stages them (plus up to kCap keys of overhang) in shared memory
-//       and sorts them stably by key.  A stable sort of whole buckets laid out
-//       in bucket order equals per-bucket insertion sort + concatenation,
-//       because bucket_index is monotone in the key.                    8n B
-//   K6  k_resolve_oversized: a super-bucket longer than a window's reach is
-//       resolved from per-window summaries (boundary, min, max); one that
-//       holds a single key value is already in arrival order, the others mark
-//       a span that the radix pipeline re-sorts ("oversized buckets go to the
-//       radix kernel").
+//   K5  k_bucket_segments: persistent CTAs, each owning the super-buckets that
+//       start in its share of the array, stage them in shared memory a few
+//       thousand keys at a time and sort them stably by key, in place.  A
+//       stable sort of whole buckets laid out in bucket order equals
+//       per-bucket insertion sort + concatenation, because bucket_index is
+//       monotone in the key.                                            8n B
+//       A super-bucket longer than the stage is oversized: one that holds a
+//       single key value is already in arrival order, the others mark a span
+//       that the radix pipeline re-sorts ("oversized buckets go to the radix
+//       kernel").
 #pragma once
 
 #include "isort_common.cuh"
@@ -163,7 +163,9 @@ template <typename K, int MODE = kWide>
 struct BucketDigitizer {
     static constexpr int kDigits = kBucketMaxDigits;
     static constexpr bool kChecks = true;
-    static constexpr bool kCheapDigit = false;
+    // narrow modes recompute the digit in the scatter phase (a multiply and a
+    // shift are cheaper than staging digits through shared memory)
+    static constexpr bool kCheapDigit = MODE != kWide;
     BucketIndexer bi;
     uint32_t shift[kBucketMaxDigits];  // digit p = (b >> shift[p]) & 255; unused: 63 (=> 0)
     uint32_t s_lo;                     // super-bucket = b >> s_lo
@@ -207,410 +209,283 @@ struct BucketState {
     unsigned long long span_lo_not;  // ~(min start) of non-constant oversized super-buckets
     unsigned long long span_hi;      // max end
     uint32_t oversized;              // non-constant oversized super-buckets
-    uint32_t n_over;                 // oversized records written by K5
-};
-
-struct OverRec {
-    unsigned long long start;  // absolute start of the trailing oversized super-bucket
-    unsigned long long kmin, kmax;  // over the part the owner staged
-    uint32_t window;
     uint32_t pad;
 };
 
-template <typename K>
-struct WindowSummary {  // per window: first super-bucket start, min/max of the keys before it
-    unsigned long long first;  // absolute, or ~0 if no super-bucket starts in the window
-    unsigned long long hmin, hmax;
-};
-
 // ------------------------------------------------------------------ K5
-template <int BLOCK, int IPT>
-struct WindowCfg {
-    static constexpr int kStage = BLOCK * IPT;  // keys staged per CTA
-    static constexpr int kWindow = kStage / 2;  // owned range; reach = 1 window (super-buckets ~2K keys)
-    static constexpr int kCap = kStage - kWindow;  // reach past the window
-    static constexpr int kWarps = BLOCK / 32;
-};
-
-constexpr int kWinDigitBits = 9;  // window sort digit width (<= 9 bits: 512 bins)
+constexpr int kWinDigitBits = 9;  // in-smem sort digit width (<= 9 bits: 512 bins)
 constexpr int kWinBins = 1 << kWinDigitBits;
-static_assert(kWinBins % 256 == 0 || kWinBins <= 256, "bins split evenly over the window CTA");
 
 template <typename K, int BLOCK, int IPT, bool VALS>
-struct WindowSmem {
+struct SegSmem {
     K keys[BLOCK * IPT];
     K keys2[BLOCK * IPT];  // ping-pong buffer of the in-smem sort
     uint32_t vals[VALS ? BLOCK * IPT : 1];
     uint32_t vals2[VALS ? BLOCK * IPT : 1];
     uint32_t cnt[BLOCK / 32][kWinBins];  // per-warp digit counters, then slot bases
     uint32_t scan_tot[BLOCK / 32];
-    unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32];
-    unsigned long long red6[6][BLOCK / 32];
-    uint32_t prev_sb;
-    int first, last, end;
+    unsigned long long red[3][BLOCK / 32];
+    unsigned long long pos[2];  // segment bounds, then the end of an oversized super-bucket
 };
-
-template <typename T>
-__device__ __forceinline__ T block_max_u64(T v, unsigned long long* red, int warps) {
-    unsigned long long x = warp_max<unsigned long long>(static_cast<unsigned long long>(v));
-    __syncthreads();
-    if (lane_id() == 0) red[threadIdx.x >> 5] = x;
-    __syncthreads();
-    x = 0;
-    for (int w = 0; w < warps; ++w) x = red[w] > x ? red[w] : x;
-    return static_cast<T>(x);
-}
-
-// Block-wide (min, max) of K values in one barrier pair.
-template <typename K>
-__device__ __forceinline__ void block_minmax(K lo, K hi, unsigned long long* ra, unsigned long long* rb, int warps,
-                                             unsigned long long& out_lo, unsigned long long& out_hi) {
-    const unsigned long long a = warp_max<unsigned long long>(~static_cast<unsigned long long>(lo));
-    const unsigned long long b = warp_max<unsigned long long>(static_cast<unsigned long long>(hi));
-    __syncthreads();
-    if (lane_id() == 0) {
-        ra[threadIdx.x >> 5] = a;
-        rb[threadIdx.x >> 5] = b;
-    }
-    __syncthreads();
-    unsigned long long x = 0, y = 0;
-    for (int w = 0; w < warps; ++w) {
-        x = ra[w] > x ? ra[w] : x;
-        y = rb[w] > y ? rb[w] : y;
-    }
-    out_lo = ~x;
-    out_hi = y;
-}
 
 // First index in [lo, hi) where the monotone predicate holds, or hi.  Called by a
 // whole warp: 32 probes per round narrow the range 32x.
 template <typename Pred>
-__device__ __forceinline__ int warp_lower_bound(int lo, int hi, Pred pred) {
-    // invariant: answer in [lo, hi]; pred(hi) is taken as true
+__device__ __forceinline__ uint64_t warp_first_true(uint64_t lo, uint64_t hi, Pred pred) {
     while (lo < hi) {
-        const int step = (hi - lo + 31) / 32;
-        const int idx = lo + static_cast<int>(lane_id()) * step;
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t idx = lo + lane_id() * step;
         const bool p = idx >= hi || pred(idx);
         const uint32_t ball = __ballot_sync(ISORT_FULL_MASK, p);
-        const int f = __ffs(ball) - 1;  // lane 31 probe may be < hi; ball can be 0
-        if (ball == 0) {
+        if (ball == 0) {  // every probe false, including lo + 31 * step < hi
             lo = lo + 31 * step + 1;
             continue;
         }
+        const int f = __ffs(ball) - 1;
         if (f == 0) return lo;
-        const int nlo = lo + (f - 1) * step + 1;
-        const int nhi = min(lo + f * step, hi);
+        const uint64_t nhi = lo + static_cast<uint64_t>(f) * step < hi ? lo + static_cast<uint64_t>(f) * step : hi;
         if (step == 1) return nhi;
-        lo = nlo;
+        lo = lo + static_cast<uint64_t>(f - 1) * step + 1;
         hi = nhi;
     }
     return hi;
 }
 
+// First super-bucket start at or after x (0 and n count as starts).  The array
+// is ordered by super-bucket after K3, so this is a lower bound: gallop from x,
+// then a 32-ary search.  Whole warp.
+template <typename K, typename Dz>
+__device__ uint64_t warp_next_start(const K* __restrict__ keys, uint64_t n, uint64_t x, const Dz& dz) {
+    if (x == 0) return 0;
+    if (x >= n) return n;
+    const uint64_t sbp = dz.super_bucket(keys[x - 1]);
+    auto differs = [&](uint64_t i) { return dz.super_bucket(keys[i]) != sbp; };
+    uint64_t lo = x, hi = n - x > 2048 ? x + 2048 : n;
+    while (hi < n && !differs(hi - 1)) {
+        lo = hi;
+        const uint64_t w = (hi - x) * 16;
+        hi = n - x > w ? x + w : n;
+    }
+    return warp_first_true(lo, hi, differs);
+}
+
+// Block reduction of (count, min, max) in one barrier pair.
+template <typename K, int BLOCK>
+__device__ __forceinline__ void block_count_minmax(uint32_t& c, K& lo, K& hi, unsigned long long (*red)[BLOCK / 32]) {
+    constexpr int kWarps = BLOCK / 32;
+    const unsigned long long v0 = warp_sum(c);
+    const unsigned long long v1 = warp_max<unsigned long long>(~static_cast<unsigned long long>(lo));
+    const unsigned long long v2 = warp_max<unsigned long long>(static_cast<unsigned long long>(hi));
+    __syncthreads();  // previous readers of red[] are done
+    if (lane_id() == 0) {
+        red[0][threadIdx.x >> 5] = v0;
+        red[1][threadIdx.x >> 5] = v1;
+        red[2][threadIdx.x >> 5] = v2;
+    }
+    __syncthreads();
+    unsigned long long a = 0, b = 0, d = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        a += red[0][w];
+        b = red[1][w] > b ? red[1][w] : b;
+        d = red[2][w] > d ? red[2][w] : d;
+    }
+    c = static_cast<uint32_t>(a);
+    lo = static_cast<K>(~b);
+    hi = static_cast<K>(d);
+}
+
+// K5: each persistent CTA owns the super-buckets that start in its share
+// [n*b/G, n*(b+1)/G) of the array (bounds moved to the next super-bucket start).
+// It walks them in steps: stage up to BLOCK*IPT keys in shared memory, sort the
+// complete super-buckets of the stage stably by key, write them back in place,
+// and continue from the first incomplete one.  A stable sort of whole buckets
+// laid out in bucket order equals per-bucket insertion sort + concatenation,
+// because bucket_index is monotone in the key.  A super-bucket longer than the
+// stage is "oversized": one holding a single key value is already in arrival
+// order; the others extend a span that the radix pipeline re-sorts.
 template <typename K, typename Dz, int BLOCK, int IPT, bool VALS>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_bucket_windows(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
-                                                          const RadixState* __restrict__ rst,
-                                                          BucketState* __restrict__ bst,
-                                                          WindowSummary<K>* __restrict__ summ,
-                                                          OverRec* __restrict__ over, Dz dz) {
-    using Cfg = WindowCfg<BLOCK, IPT>;
-    using Smem = WindowSmem<K, BLOCK, IPT, VALS>;
-    constexpr int kStage = Cfg::kStage, kWindow = Cfg::kWindow, kWarps = Cfg::kWarps;
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+    k_bucket_segments(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
+                      const RadixState* __restrict__ rst, BucketState* __restrict__ bst, Dz dz) {
+    using Smem = SegSmem<K, BLOCK, IPT, VALS>;
+    constexpr int kStage = BLOCK * IPT, kWarps = BLOCK / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     if (rst->descents == 0 || rst->first_bad != 0) return;  // sorted input / range error: nothing to do
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
-    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kWindow;
-    const int avail = static_cast<int>((n - w0 < static_cast<uint64_t>(kStage) ? n - w0 : static_cast<uint64_t>(kStage)));
-    const int wlen = min(kWindow, avail);
-
-#ifdef ISORT_PHASE_TIMING
-    long long t0 = clock64(), t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    unsigned long long* prof = const_cast<unsigned long long*>(rst->prof);
-#define WTICK(v) v = clock64()
-#define WFLUSH(k)                                                                      \
-    if (tid == 0) {                                                                    \
-        const long long tn = clock64();                                                \
-        atomicAdd(prof + 8, (unsigned long long)((t1 ? t1 : tn) - t0));               \
-        if (t1) atomicAdd(prof + 9, (unsigned long long)((t2 ? t2 : tn) - t1));       \
-        if (t2) atomicAdd(prof + 10, (unsigned long long)((t3 ? t3 : tn) - t2));      \
-        if (t3) atomicAdd(prof + 11, (unsigned long long)((t4 ? t4 : tn) - t3));      \
-        if (t4) atomicAdd(prof + 12, (unsigned long long)(tn - t4));                  \
-        atomicAdd(prof + 13 + (k), 1ull);                                              \
-    }
-#else
-#define WTICK(v)
-#define WFLUSH(k)
-#endif
-    // ---- stage [w0, w0 + avail); super-bucket id (low 32 bits: adjacent ids differ
-    // by far less than 2^32, so equality is exact) kept per position in sm.keys2
-    uint32_t* sbuf = reinterpret_cast<uint32_t*>(sm.keys2);
-    {
-        K stage[IPT];
-        uint32_t vstage[VALS ? IPT : 1];
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int j = tid + i * BLOCK;
-            if (j < avail) {
-                stage[i] = keys[w0 + j];
-                if (VALS) vstage[i] = vals[w0 + j];
-            }
-        }
-        if (tid == 0) sm.prev_sb = w0 ? static_cast<uint32_t>(dz.super_bucket(keys[w0 - 1])) : 0u;
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int j = tid + i * BLOCK;
-            if (j < avail) {
-                sm.keys[j] = stage[i];
-                sbuf[j] = static_cast<uint32_t>(dz.super_bucket(stage[i]));
-                if (VALS) sm.vals[j] = vstage[i];
-            }
-        }
+    if (warp < 2) {
+        const uint64_t x = n * (blockIdx.x + static_cast<uint64_t>(warp)) / gridDim.x;
+        const uint64_t p = warp_next_start(keys, n, x, dz);
+        if (lane == 0) sm.pos[warp] = p;
     }
     __syncthreads();
-    WTICK(t1);
-    // ---- super-bucket starts (all threads): first/last start in [0, wlen), first start in [wlen, avail)
-    {
-        int my_first = 0x7fffffff, my_last = -1, my_end = 0x7fffffff;
+    uint64_t pos = sm.pos[0];
+    const uint64_t seg_hi = sm.pos[1];
+
+    while (pos < seg_hi) {
+        const int len = seg_hi - pos < static_cast<uint64_t>(kStage) ? static_cast<int>(seg_hi - pos) : kStage;
+        const bool tail = pos + len == seg_hi;  // ends on a super-bucket start: all complete
+        const uint64_t sb_last = tail ? ~0ull : dz.super_bucket(keys[pos + len - 1]);
+        // ---- stage; count the keys before the last (possibly incomplete) super-bucket
+        uint32_t ls = 0;
+        K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
+        {
+            K kr[IPT];
+            uint32_t vr[VALS ? IPT : 1];
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int j = tid + i * BLOCK;
-            if (j < avail) {
-                const bool start = (w0 + j == 0) || sbuf[j] != (j ? sbuf[j - 1] : sm.prev_sb);
-                if (start) {
-                    if (j < wlen) {
-                        my_first = min(my_first, j);
-                        my_last = max(my_last, j);
-                    } else {
-                        my_end = min(my_end, j);
+            for (int i = 0; i < IPT; ++i) {
+                const int j = tid + i * BLOCK;
+                if (j < len) {
+                    kr[i] = keys[pos + j];
+                    if (VALS) vr[i] = vals[pos + j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const int j = tid + i * BLOCK;
+                if (j < len) {
+                    sm.keys[j] = kr[i];
+                    if (VALS) sm.vals[j] = vr[i];
+                    if (tail || dz.super_bucket(kr[i]) != sb_last) {
+                        ++ls;
+                        kmin = kr[i] < kmin ? kr[i] : kmin;
+                        kmax = kr[i] > kmax ? kr[i] : kmax;
                     }
                 }
             }
         }
-        my_first = __reduce_min_sync(ISORT_FULL_MASK, my_first);
-        my_last = __reduce_max_sync(ISORT_FULL_MASK, my_last);
-        my_end = __reduce_min_sync(ISORT_FULL_MASK, my_end);
-        if (tid == 0) {
-            sm.first = 0x7fffffff;
-            sm.last = -1;
-            sm.end = 0x7fffffff;
-        }
-        __syncthreads();
-        if (lane == 0) {
-            if (my_first != 0x7fffffff) atomicMin(&sm.first, my_first);
-            if (my_last >= 0) atomicMax(&sm.last, my_last);
-            if (my_end != 0x7fffffff) atomicMin(&sm.end, my_end);
-        }
-        __syncthreads();
-    }
-    WTICK(t2);
-    const int first = min(sm.first, wlen);
-    int end = min(sm.end, avail);
-    const bool oversized = first < wlen && end == avail && w0 + avail < n;
-    const int ostart = sm.last;
-    if (oversized) end = ostart;  // the trailing super-bucket is resolved by K6
-    // ---- one block reduction: head (before `first`), sort range, oversized tail
-    K hmin = static_cast<K>(~static_cast<K>(0)), hmax = 0, rmin = hmin, rmax = 0, omin = hmin, omax = 0;
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int j = tid + i * BLOCK;
-        if (j < avail) {
-            const K k = sm.keys[j];
-            if (j < first) {
-                hmin = k < hmin ? k : hmin;
-                hmax = k > hmax ? k : hmax;
-            } else if (j < end) {
-                rmin = k < rmin ? k : rmin;
-                rmax = k > rmax ? k : rmax;
-            } else if (oversized) {
-                omin = k < omin ? k : omin;
-                omax = k > omax ? k : omax;
+        block_count_minmax<K, BLOCK>(ls, kmin, kmax, sm.red);
+        if (ls == 0) {  // the whole stage is one super-bucket
+            if (warp == 0) {
+                const uint64_t e = warp_next_start(keys, n, pos + len, dz);
+                if (lane == 0) sm.pos[0] = e;
+            }
+            __syncthreads();
+            const uint64_t e = sm.pos[0];
+            kmin = static_cast<K>(~static_cast<K>(0));
+            kmax = 0;
+            if (e == pos + static_cast<uint64_t>(len)) {  // ends exactly with the stage
+                ls = len;
+                for (int j = tid; j < len; j += BLOCK) {
+                    const K k = sm.keys[j];
+                    kmin = k < kmin ? k : kmin;
+                    kmax = k > kmax ? k : kmax;
+                }
+                uint32_t dummy = 0;
+                block_count_minmax<K, BLOCK>(dummy, kmin, kmax, sm.red);
+            } else {  // oversized: constant (nothing to do) or a span for the radix fallback
+                for (uint64_t i = pos + tid; i < e; i += BLOCK) {
+                    const K k = keys[i];
+                    kmin = k < kmin ? k : kmin;
+                    kmax = k > kmax ? k : kmax;
+                }
+                uint32_t dummy = 0;
+                block_count_minmax<K, BLOCK>(dummy, kmin, kmax, sm.red);
+                if (tid == 0 && kmin != kmax) {
+                    atomicAdd(&bst->oversized, 1u);
+                    atomicMax(&bst->span_lo_not, ~static_cast<unsigned long long>(pos));
+                    atomicMax(&bst->span_hi, static_cast<unsigned long long>(e));
+                }
+                pos = e;
+                __syncthreads();
+                continue;
             }
         }
-    }
-    {
-        unsigned long long v[6] = {~static_cast<unsigned long long>(hmin), hmax, ~static_cast<unsigned long long>(rmin),
-                                   rmax, ~static_cast<unsigned long long>(omin), omax};
-#pragma unroll
-        for (int q = 0; q < 6; ++q) v[q] = warp_max<unsigned long long>(v[q]);
-        if (lane == 0) {
-#pragma unroll
-            for (int q = 0; q < 6; ++q) sm.red6[q][warp] = v[q];
+        if (kmin == kmax) {  // one key value (or one key): arrival order is the answer, in place
+            pos += ls;
+            __syncthreads();
+            continue;
         }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            unsigned long long x = 0;
-            for (int w = 0; w < kWarps; ++w) x = sm.red6[q][w] > x ? sm.red6[q][w] : x;
-            v[q] = x;
-        }
-        hmin = static_cast<K>(~v[0]);
-        hmax = static_cast<K>(v[1]);
-        rmin = static_cast<K>(~v[2]);
-        rmax = static_cast<K>(v[3]);
-        omin = static_cast<K>(~v[4]);
-        omax = static_cast<K>(v[5]);
-    }
-    if (tid == 0) {
-        summ[blockIdx.x].first = first < wlen ? w0 + first : ~0ull;
-        summ[blockIdx.x].hmin = first > 0 ? static_cast<unsigned long long>(hmin) : ~0ull;
-        summ[blockIdx.x].hmax = first > 0 ? static_cast<unsigned long long>(hmax) : 0ull;
-        if (oversized) {
-            const uint32_t r = atomicAdd(&bst->n_over, 1u);
-            over[r].start = w0 + ostart;
-            over[r].kmin = omin;
-            over[r].kmax = omax;
-            over[r].window = blockIdx.x;
-        }
-    }
-    WTICK(t3);
-    if (first >= wlen) {  // no super-bucket starts here
-        WFLUSH(0);
-        return;
-    }
-    const int len = end - first;
-    if (len <= 1) {
-        WFLUSH(1);
-        return;
-    }
 
-    // ---- stable in-smem LSD sort of sm.keys[first, end) by (key - min), r-bit digits
-    // Same rank primitive as the one-sweep pass: per-warp counters pre-scanned into
-    // slot bases, slot = atomicAdd (lane-ordered, program-ordered => stable).
-    const K kmin = rmin, kmax = rmax;
-    WTICK(t4);
-    if (kmin == kmax) {  // one key value: arrival order is the answer
-        WFLUSH(1);
-        return;
-    }
-    const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
-    const int passes = (bits + kWinDigitBits - 1) / kWinDigitBits;
-    const int r = (bits + passes - 1) / passes;
-    const uint32_t nbins = 1u << r, mask = nbins - 1u;
-    K* ka = sm.keys + first;
-    K* kb = sm.keys2;
-    uint32_t* va = sm.vals + first;
-    uint32_t* vb = sm.vals2;
-    // items per thread sized to this window's range, so every warp has work
-    const int ipt = (len + BLOCK - 1) / BLOCK;
-    const int wofs = warp * 32 * ipt + static_cast<int>(lane);
-    for (int pass = 0; pass < passes; ++pass) {
-        const uint32_t shift = static_cast<uint32_t>(pass * r);
-        for (int i = tid; i < kWarps * static_cast<int>(nbins); i += BLOCK)
-            sm.cnt[i / static_cast<int>(nbins)][i % static_cast<int>(nbins)] = 0;
-        __syncthreads();
-        uint32_t* wc = sm.cnt[warp];
+        // ---- stable in-smem LSD sort of sm.keys[0, ls) by (key - min), r-bit digits
+        // Same rank primitive as the one-sweep pass: per-warp counters pre-scanned into
+        // slot bases, slot = atomicAdd (lane-ordered, program-ordered => stable).
+        const int len_s = static_cast<int>(ls);
+        const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
+        const int passes = (bits + kWinDigitBits - 1) / kWinDigitBits;
+        const int r = (bits + passes - 1) / passes;
+        const uint32_t nbins = 1u << r, mask = nbins - 1u;
+        K* ka = sm.keys;
+        K* kb = sm.keys2;
+        uint32_t* va = sm.vals;
+        uint32_t* vb = sm.vals2;
+        const int ipt = (len_s + BLOCK - 1) / BLOCK;  // items per thread sized to this stage
+        const int wofs = warp * 32 * ipt + static_cast<int>(lane);
+        for (int pass = 0; pass < passes; ++pass) {
+            const uint32_t shift = static_cast<uint32_t>(pass * r);
+            for (int i = tid; i < kWarps * static_cast<int>(nbins); i += BLOCK)
+                sm.cnt[i / static_cast<int>(nbins)][i % static_cast<int>(nbins)] = 0;
+            __syncthreads();
+            uint32_t* wc = sm.cnt[warp];
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int o = wofs + i * 32;
-            if (i < ipt && o < len)
-                atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
-        }
-        __syncthreads();
-        // bins [tid*BPT, tid*BPT + BPT): totals over warps, block scan over bins, per-warp bases
-        constexpr int BPT = kWinBins / BLOCK > 0 ? kWinBins / BLOCK : 1;
-        uint32_t btot[BPT], tsum = 0;
-#pragma unroll
-        for (int q = 0; q < BPT; ++q) {
-            const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
-            uint32_t t = 0;
-            if (b < nbins) {
-#pragma unroll 4
-                for (int w = 0; w < kWarps; ++w) t += sm.cnt[w][b];
+            for (int i = 0; i < IPT; ++i) {
+                const int o = wofs + i * 32;
+                if (i < ipt && o < len_s)
+                    atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
             }
-            btot[q] = t;
-            tsum += t;
-        }
-        const uint32_t inc = warp_inclusive_scan(tsum);
-        if (lane == 31) sm.scan_tot[warp] = inc;
-        __syncthreads();
-        {
-            uint32_t base = inc - tsum;
-            for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
+            __syncthreads();
+            // bins [tid*BPT, tid*BPT + BPT): totals over warps, block scan over bins, per-warp bases
+            constexpr int BPT = kWinBins / BLOCK > 0 ? kWinBins / BLOCK : 1;
+            uint32_t btot[BPT], tsum = 0;
 #pragma unroll
             for (int q = 0; q < BPT; ++q) {
                 const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
+                uint32_t t = 0;
                 if (b < nbins) {
-                    uint32_t bb = base;
 #pragma unroll 4
-                    for (int w = 0; w < kWarps; ++w) {
-                        const uint32_t v = sm.cnt[w][b];
-                        sm.cnt[w][b] = bb;
-                        bb += v;
-                    }
+                    for (int w = 0; w < kWarps; ++w) t += sm.cnt[w][b];
                 }
-                base += btot[q];
+                btot[q] = t;
+                tsum += t;
             }
-        }
-        __syncthreads();
+            const uint32_t inc = warp_inclusive_scan(tsum);
+            if (lane == 31) sm.scan_tot[warp] = inc;
+            __syncthreads();
+            {
+                uint32_t base = inc - tsum;
+                for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int o = wofs + i * 32;
-            if (i < ipt && o < len) {
-                const K k = ka[o];
-                const uint32_t slot = atomicAdd(&wc[static_cast<uint32_t>((k - kmin) >> shift) & mask], 1u);
-                kb[slot] = k;
-                if (VALS) vb[slot] = va[o];
+                for (int q = 0; q < BPT; ++q) {
+                    const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
+                    if (b < nbins) {
+                        uint32_t bb = base;
+#pragma unroll 4
+                        for (int w = 0; w < kWarps; ++w) {
+                            const uint32_t v = sm.cnt[w][b];
+                            sm.cnt[w][b] = bb;
+                            bb += v;
+                        }
+                    }
+                    base += btot[q];
+                }
             }
-        }
-        __syncthreads();
-        K* tk = ka;
-        ka = kb;
-        kb = tk;
-        uint32_t* tv = va;
-        va = vb;
-        vb = tv;
-    }
-    for (int j = tid; j < len; j += BLOCK) {
-        keys[w0 + first + j] = ka[j];
-        if (VALS) vals[w0 + first + j] = va[j];
-    }
-    WFLUSH(2);
-#undef WTICK
-#undef WFLUSH
-}
-
-// ------------------------------------------------------------------ K6
-// One CTA per oversized record: walk the following windows' summaries until a
-// super-bucket start appears; combine min/max.  Non-constant => mark the span.
-template <typename K, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_resolve_oversized(const WindowSummary<K>* __restrict__ summ,
-                                                             uint32_t num_windows, const OverRec* __restrict__ over,
-                                                             BucketState* __restrict__ bst, uint64_t n) {
-    __shared__ unsigned long long red_a[BLOCK / 32], red_b[BLOCK / 32], red_c[BLOCK / 32];
-    const uint32_t nrec = bst->n_over;
-    for (uint32_t r = blockIdx.x; r < nrec; r += gridDim.x) {
-        const OverRec rec = over[r];
-        unsigned long long kmin = rec.kmin, kmax = rec.kmax;
-        unsigned long long end = n;
-        for (uint32_t base = rec.window + 1; base < num_windows; base += BLOCK) {
-            const uint32_t w = base + threadIdx.x;
-            unsigned long long f = ~0ull, hmin = ~0ull, hmax = 0;
-            if (w < num_windows) {
-                f = summ[w].first;
-                hmin = summ[w].hmin;
-                hmax = summ[w].hmax;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const int o = wofs + i * 32;
+                if (i < ipt && o < len_s) {
+                    const K k = ka[o];
+                    const uint32_t slot = atomicAdd(&wc[static_cast<uint32_t>((k - kmin) >> shift) & mask], 1u);
+                    kb[slot] = k;
+                    if (VALS) vb[slot] = va[o];
+                }
             }
-            // first window (lowest index) with a start
-            unsigned long long fw = f != ~0ull ? static_cast<unsigned long long>(w) : ~0ull;
-            fw = ~block_max_u64(~fw, red_c, BLOCK / 32);
-            const bool take = w < num_windows && static_cast<unsigned long long>(w) <= fw;
-            const unsigned long long a = block_max_u64(take ? ~hmin : 0ull, red_a, BLOCK / 32);
-            const unsigned long long b = block_max_u64(take ? hmax : 0ull, red_b, BLOCK / 32);
-            kmin = (~a) < kmin ? ~a : kmin;
-            kmax = b > kmax ? b : kmax;
-            if (fw != ~0ull) {
-                end = summ[fw].first;
-                break;
-            }
+            __syncthreads();
+            K* tk = ka;
+            ka = kb;
+            kb = tk;
+            uint32_t* tv = va;
+            va = vb;
+            vb = tv;
         }
-        if (threadIdx.x == 0 && kmin != kmax) {
-            atomicAdd(&bst->oversized, 1u);
-            atomicMax(&bst->span_lo_not, ~rec.start);
-            atomicMax(&bst->span_hi, end);
+        for (int j = tid; j < len_s; j += BLOCK) {
+            keys[pos + j] = ka[j];
+            if (VALS) vals[pos + j] = va[j];
         }
+        pos += ls;
         __syncthreads();
     }
 }

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -434,30 +435,41 @@ __global__ void k_is_sorted_u32(const uint32_t* __restrict__ keys, uint64_t n, u
 
 
 // ------------------------------------------------------------- bucket sort
-constexpr int kWinBlock = 512;
-constexpr int kWinIpt = 16;
+constexpr int kSegBlock = 512;
+constexpr int kSegIpt = 16;
 
 struct BucketLayout {
     RadixLayout r;
-    size_t bstate = 0, summ = 0, over = 0, total = 0;
-    uint32_t windows = 0;
+    size_t bstate = 0, total = 0;
 };
 
 template <typename K>
 BucketLayout bucket_layout(uint64_t n, bool vals) {
     BucketLayout L;
     L.r = radix_layout<K>(n, vals);  // state, lookback (>= 3 digit slots), alt buffers
-    L.windows = static_cast<uint32_t>((n + WindowCfg<kWinBlock, kWinIpt>::kWindow - 1) /
-                                      WindowCfg<kWinBlock, kWinIpt>::kWindow);
     size_t off = L.r.total;
     L.bstate = off;
     off += align_up(sizeof(BucketState));
-    L.summ = off;
-    off += align_up(static_cast<size_t>(L.windows) * sizeof(WindowSummary<K>));
-    L.over = off;
-    off += align_up(static_cast<size_t>(L.windows) * sizeof(OverRec));
     L.total = off;
     return L;
+}
+
+// K5 launch: persistent, as many CTAs as fit (at most one per ~4K keys).
+template <typename K, typename Dz, bool VALS>
+void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, BucketState* bst, const Dz& dz,
+                     cudaStream_t s) {
+    using Smem = SegSmem<K, kSegBlock, kSegIpt, VALS>;
+    auto* kern = k_bucket_segments<K, Dz, kSegBlock, kSegIpt, VALS>;
+    set_max_smem_once(kern, sizeof(Smem));
+    static thread_local std::map<const void*, int> occ;
+    int& per_sm = occ[reinterpret_cast<const void*>(kern)];
+    if (per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSegBlock, sizeof(Smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const uint64_t want = (n + 4095) / 4096;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
+    kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);
 }
 
 template <typename K, int MODE>
@@ -500,8 +512,6 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
-    auto* summ = reinterpret_cast<WindowSummary<K>*>(t + L.summ);
-    auto* over = reinterpret_cast<OverRec*>(t + L.over);
     const BucketDigitizer<K, MODE> dz = BucketDigitizer<K, MODE>::make(n, bound);
     const bool iota = vmode == ISORT_VALS_IOTA;
 
@@ -511,22 +521,12 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
                                                     L.r.tiles, dz, true, true, s);
     if (rc) return rc;
     ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
-    if (vals) {
-        using Smem = WindowSmem<K, kWinBlock, kWinIpt, true>;
-        auto* kern = k_bucket_windows<K, BucketDigitizer<K, MODE>, kWinBlock, kWinIpt, true>;
-        set_max_smem_once(kern, sizeof(Smem));
-        kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, vout, n, st, bst, summ, over, dz);
-    } else {
-        using Smem = WindowSmem<K, kWinBlock, kWinIpt, false>;
-        auto* kern = k_bucket_windows<K, BucketDigitizer<K, MODE>, kWinBlock, kWinIpt, false>;
-        set_max_smem_once(kern, sizeof(Smem));
-        kern<<<L.windows, kWinBlock, sizeof(Smem), s>>>(kout, nullptr, n, st, bst, summ, over, dz);
-    }
-    prof_mark(s, "windows");
-    k_resolve_oversized<K, 256><<<L.windows < 4u * kNumSMs ? L.windows : 4u * kNumSMs, 256, 0, s>>>(
-        summ, L.windows, over, bst, n);
-    prof_mark(s, "resolve");
-    launched(2);
+    if (vals)
+        launch_segments<K, BucketDigitizer<K, MODE>, true>(kout, vout, n, st, bst, dz, s);
+    else
+        launch_segments<K, BucketDigitizer<K, MODE>, false>(kout, nullptr, n, st, bst, dz, s);
+    prof_mark(s, "segments");
+    launched(1);
     ISORT_CUDA_TRY(cudaGetLastError());
 
     // one small read-back: range error and oversized span

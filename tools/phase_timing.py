@@ -53,19 +53,3 @@ acc = temp[off:off + 128].cpu().numpy().view(np.uint64)
 tiles = int(acc[3])
 print(f"tiles={tiles}  cycles/tile: phase1={acc[0] / tiles:.0f}  totals+lookback={acc[1] / tiles:.0f}"
       f"  bases+phase2={acc[2] / tiles:.0f}")
-
-if "--bucket" in sys.argv:
-    from paper_1206_3511_b200 import device
-
-    sorter = device.Sorter(n, 4, "bucket", None, range_bound=(1 << 32) - 1)
-    lib2 = lib
-    tb = lib2.isort_bucket_temp_bytes(n, 4, 0)
-    temp = torch.empty(tb, dtype=torch.uint8, device="cuda")
-    assert lib2.isort_bucket_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, (1 << 32) - 1, 0,
-                                      temp.data_ptr(), tb, s) == 0
-    torch.cuda.synchronize()
-    acc = temp[off:off + 128].cpu().numpy().view(np.uint64)
-    wins = int(acc[13] + acc[14] + acc[15])
-    print(f"windows={wins} (no-start={acc[13]}, trivial={acc[14]}, sorted={acc[15]})  cycles/window: "
-          f"stage={acc[8] / wins:.0f} search={acc[9] / wins:.0f} head={acc[10] / max(1, acc[14] + acc[15]):.0f} "
-          f"minmax={acc[11] / max(1, acc[15]):.0f} sort+write={acc[12] / max(1, acc[15]):.0f}")
