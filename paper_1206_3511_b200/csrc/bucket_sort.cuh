@@ -213,8 +213,10 @@ struct BucketState {
 };
 
 // ------------------------------------------------------------------ K5
-constexpr int kWinDigitBits = 9;  // in-smem sort digit width (<= 9 bits: 512 bins)
-constexpr int kWinBins = 1 << kWinDigitBits;
+// In-smem sort: up to 10-bit digits, two 16-bit counters per 32-bit word (a
+// stage holds < 2^16 keys, so a half never carries into the other).
+constexpr int kSegDigitBits = 10;
+constexpr int kSegWords = 1 << (kSegDigitBits - 1);
 
 template <typename K, int BLOCK, int IPT, bool VALS>
 struct SegSmem {
@@ -222,10 +224,11 @@ struct SegSmem {
     K keys2[BLOCK * IPT];  // ping-pong buffer of the in-smem sort
     uint32_t vals[VALS ? BLOCK * IPT : 1];
     uint32_t vals2[VALS ? BLOCK * IPT : 1];
-    uint32_t cnt[BLOCK / 32][kWinBins];  // per-warp digit counters, then slot bases
+    alignas(16) uint32_t cnt[BLOCK / 32][kSegWords];  // per-warp packed digit counters, then slot bases
     uint32_t scan_tot[BLOCK / 32];
-    unsigned long long red[3][BLOCK / 32];
+    unsigned long long red[2][BLOCK / 32];
     unsigned long long pos[2];  // segment bounds, then the end of an oversized super-bucket
+    int ls;                     // start of the stage's last super-bucket
 };
 
 // First index in [lo, hi) where the monotone predicate holds, or hi.  Called by a
@@ -269,30 +272,155 @@ __device__ uint64_t warp_next_start(const K* __restrict__ keys, uint64_t n, uint
     return warp_first_true(lo, hi, differs);
 }
 
-// Block reduction of (count, min, max) in one barrier pair.
+// Count / rank steps of seg_lsd for one warp's IPT x 32 positions; FULL: all in range.
+template <bool FULL, typename K, int IPT>
+__device__ __forceinline__ void seg_count(const K* ka, int obase, int len, K kmin, uint32_t shift, uint32_t mask,
+                                          uint32_t* wc, K (&kv)[IPT]) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int o = obase + i * 32;
+        if (FULL || o < len) {
+            kv[i] = ka[o];
+            const uint32_t d = static_cast<uint32_t>((kv[i] - kmin) >> shift) & mask;
+            atomicAdd(&wc[d >> 1], 1u << ((d & 1u) << 4));
+        }
+    }
+}
+
+template <bool FULL, typename K, int IPT, bool VALS>
+__device__ __forceinline__ void seg_rank(K* kb, const uint32_t* va, uint32_t* vb, int obase, int len, K kmin,
+                                         uint32_t shift, uint32_t mask, uint32_t* wc, const K (&kv)[IPT]) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int o = obase + i * 32;
+        if (FULL || o < len) {
+            const uint32_t d = static_cast<uint32_t>((kv[i] - kmin) >> shift) & mask;
+            const uint32_t h = (d & 1u) << 4;
+            const uint32_t slot = (atomicAdd(&wc[d >> 1], 1u << h) >> h) & 0xFFFFu;
+            kb[slot] = kv[i];
+            if (VALS) vb[slot] = va[o];
+        }
+    }
+}
+
+// Stage keys[pos, pos + len) (and payload) into shared memory; min/max of the keys.
+template <bool FULL, typename K, int BLOCK, int IPT, bool VALS>
+__device__ __forceinline__ void seg_stage(const K* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t pos,
+                                          int len, K* skeys, uint32_t* svals, K& kmin, K& kmax) {
+    K kr[IPT];
+    uint32_t vr[VALS ? IPT : 1];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int j = static_cast<int>(threadIdx.x) + i * BLOCK;
+        if (FULL || j < len) {
+            kr[i] = keys[pos + j];
+            if (VALS) vr[i] = vals[pos + j];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int j = static_cast<int>(threadIdx.x) + i * BLOCK;
+        if (FULL || j < len) {
+            skeys[j] = kr[i];
+            if (VALS) svals[j] = vr[i];
+            kmin = kr[i] < kmin ? kr[i] : kmin;
+            kmax = kr[i] > kmax ? kr[i] : kmax;
+        }
+    }
+}
+
+// Block-wide (min, max), two barriers; the final step is a warp reduction.
 template <typename K, int BLOCK>
-__device__ __forceinline__ void block_count_minmax(uint32_t& c, K& lo, K& hi, unsigned long long (*red)[BLOCK / 32]) {
+__device__ __forceinline__ void block_minmax2(K& lo, K& hi, unsigned long long (*red)[BLOCK / 32]) {
     constexpr int kWarps = BLOCK / 32;
-    const unsigned long long v0 = warp_sum(c);
-    const unsigned long long v1 = warp_max<unsigned long long>(~static_cast<unsigned long long>(lo));
-    const unsigned long long v2 = warp_max<unsigned long long>(static_cast<unsigned long long>(hi));
+    const uint32_t lane = lane_id();
+    unsigned long long a = warp_max<unsigned long long>(~static_cast<unsigned long long>(lo));
+    unsigned long long b = warp_max<unsigned long long>(static_cast<unsigned long long>(hi));
     __syncthreads();  // previous readers of red[] are done
-    if (lane_id() == 0) {
-        red[0][threadIdx.x >> 5] = v0;
-        red[1][threadIdx.x >> 5] = v1;
-        red[2][threadIdx.x >> 5] = v2;
+    if (lane == 0) {
+        red[0][threadIdx.x >> 5] = a;
+        red[1][threadIdx.x >> 5] = b;
     }
     __syncthreads();
-    unsigned long long a = 0, b = 0, d = 0;
+    a = lane < static_cast<uint32_t>(kWarps) ? red[0][lane] : 0ull;
+    b = lane < static_cast<uint32_t>(kWarps) ? red[1][lane] : 0ull;
+    a = warp_max<unsigned long long>(a);
+    b = warp_max<unsigned long long>(b);
+    lo = static_cast<K>(~a);
+    hi = static_cast<K>(b);
+}
+
+// Stable LSD sort of ka[0, len) (payload va) in shared memory by key - kmin,
+// `passes` r-bit digits (r <= kSegDigitBits); ka/kb (va/vb) swap each pass.
+// Rank primitive of the one-sweep pass: per-warp counters pre-scanned into slot
+// bases, slot = atomicAdd (lane-ordered, program-ordered => stable).  Warp w
+// owns positions [w*32*IPT, (w+1)*32*IPT); keys stay in registers between the
+// count and the rank step.
+template <typename K, int BLOCK, int IPT, bool VALS>
+__device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K*& ka, K*& kb, uint32_t*& va,
+                                        uint32_t*& vb, int len, K kmin, int passes, int r) {
+    constexpr int kWarps = BLOCK / 32;
+    static_assert(kSegWords <= BLOCK, "one counter word per thread in the scan");
+    static_assert(BLOCK * IPT < 65536, "16-bit counters");
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t nwords = 1u << (r - 1), mask = (1u << r) - 1u;
+    const int obase = warp * 32 * IPT + static_cast<int>(lane);
+    uint32_t* wc = sm.cnt[warp];
+    for (int pass = 0; pass < passes; ++pass) {
+        const uint32_t shift = static_cast<uint32_t>(pass * r);
+        {
+            uint4* c4 = reinterpret_cast<uint4*>(&sm.cnt[0][0]);
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        a += red[0][w];
-        b = red[1][w] > b ? red[1][w] : b;
-        d = red[2][w] > d ? red[2][w] : d;
+            for (int i = tid; i < kWarps * kSegWords / 4; i += BLOCK) c4[i] = make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        K kv[IPT];
+        const bool wfull = obase - static_cast<int>(lane) + 32 * IPT <= len;  // warp-uniform
+        if (wfull)
+            seg_count<true, K, IPT>(ka, obase, len, kmin, shift, mask, wc, kv);
+        else
+            seg_count<false, K, IPT>(ka, obase, len, kmin, shift, mask, wc, kv);
+        __syncthreads();
+        // thread t owns counter word t (digits 2t, 2t+1): totals over warps, scan, per-warp bases
+        uint32_t lo = 0, hi = 0;
+        if (static_cast<uint32_t>(tid) < nwords) {
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t v = sm.cnt[w][tid];
+                lo += v & 0xFFFFu;
+                hi += v >> 16;
+            }
+        }
+        const uint32_t tsum = lo + hi;
+        const uint32_t inc = warp_inclusive_scan(tsum);
+        if (lane == 31) sm.scan_tot[warp] = inc;
+        __syncthreads();
+        if (static_cast<uint32_t>(tid) < nwords) {
+            uint32_t base = inc - tsum;
+            for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
+            uint32_t blo = base, bhi = base + lo;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t v = sm.cnt[w][tid];
+                sm.cnt[w][tid] = blo | (bhi << 16);
+                blo += v & 0xFFFFu;
+                bhi += v >> 16;
+            }
+        }
+        __syncthreads();
+        if (wfull)
+            seg_rank<true, K, IPT, VALS>(kb, va, vb, obase, len, kmin, shift, mask, wc, kv);
+        else
+            seg_rank<false, K, IPT, VALS>(kb, va, vb, obase, len, kmin, shift, mask, wc, kv);
+        __syncthreads();
+        K* tk = ka;
+        ka = kb;
+        kb = tk;
+        uint32_t* tv = va;
+        va = vb;
+        vb = tv;
     }
-    c = static_cast<uint32_t>(a);
-    lo = static_cast<K>(~b);
-    hi = static_cast<K>(d);
 }
 
 // K5: each persistent CTA owns the super-buckets that start in its share
@@ -309,7 +437,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     k_bucket_segments(K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
                       const RadixState* __restrict__ rst, BucketState* __restrict__ bst, Dz dz) {
     using Smem = SegSmem<K, BLOCK, IPT, VALS>;
-    constexpr int kStage = BLOCK * IPT, kWarps = BLOCK / 32;
+    constexpr int kStage = BLOCK * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     if (rst->descents == 0 || rst->first_bad != 0) return;  // sorted input / range error: nothing to do
@@ -328,36 +456,28 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     while (pos < seg_hi) {
         const int len = seg_hi - pos < static_cast<uint64_t>(kStage) ? static_cast<int>(seg_hi - pos) : kStage;
         const bool tail = pos + len == seg_hi;  // ends on a super-bucket start: all complete
-        const uint64_t sb_last = tail ? ~0ull : dz.super_bucket(keys[pos + len - 1]);
-        // ---- stage; count the keys before the last (possibly incomplete) super-bucket
-        uint32_t ls = 0;
+        // ---- stage; min/max of the stage (a superset of the sorted part is fine:
+        // the tail super-bucket's keys are all larger than the complete ones')
         K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
-        {
-            K kr[IPT];
-            uint32_t vr[VALS ? IPT : 1];
-#pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const int j = tid + i * BLOCK;
-                if (j < len) {
-                    kr[i] = keys[pos + j];
-                    if (VALS) vr[i] = vals[pos + j];
-                }
+        if (len == kStage)
+            seg_stage<true, K, BLOCK, IPT, VALS>(keys, vals, pos, len, sm.keys, sm.vals, kmin, kmax);
+        else
+            seg_stage<false, K, BLOCK, IPT, VALS>(keys, vals, pos, len, sm.keys, sm.vals, kmin, kmax);
+        __syncthreads();
+        // ---- ls = start of the last (possibly incomplete) super-bucket: a lower bound
+        // over the staged keys, which are ordered by super-bucket
+        if (warp == 0) {
+            int l = len;
+            if (!tail) {
+                const uint64_t sbl = dz.super_bucket(sm.keys[len - 1]);
+                l = static_cast<int>(warp_first_true(0, static_cast<uint64_t>(len), [&](uint64_t j) {
+                    return dz.super_bucket(sm.keys[j]) == sbl;
+                }));
             }
-#pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const int j = tid + i * BLOCK;
-                if (j < len) {
-                    sm.keys[j] = kr[i];
-                    if (VALS) sm.vals[j] = vr[i];
-                    if (tail || dz.super_bucket(kr[i]) != sb_last) {
-                        ++ls;
-                        kmin = kr[i] < kmin ? kr[i] : kmin;
-                        kmax = kr[i] > kmax ? kr[i] : kmax;
-                    }
-                }
-            }
+            if (lane == 0) sm.ls = l;
         }
-        block_count_minmax<K, BLOCK>(ls, kmin, kmax, sm.red);
+        block_minmax2<K, BLOCK>(kmin, kmax, sm.red);
+        int ls = sm.ls;
         if (ls == 0) {  // the whole stage is one super-bucket
             if (warp == 0) {
                 const uint64_t e = warp_next_start(keys, n, pos + len, dz);
@@ -365,25 +485,17 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             }
             __syncthreads();
             const uint64_t e = sm.pos[0];
-            kmin = static_cast<K>(~static_cast<K>(0));
-            kmax = 0;
             if (e == pos + static_cast<uint64_t>(len)) {  // ends exactly with the stage
                 ls = len;
-                for (int j = tid; j < len; j += BLOCK) {
-                    const K k = sm.keys[j];
-                    kmin = k < kmin ? k : kmin;
-                    kmax = k > kmax ? k : kmax;
-                }
-                uint32_t dummy = 0;
-                block_count_minmax<K, BLOCK>(dummy, kmin, kmax, sm.red);
             } else {  // oversized: constant (nothing to do) or a span for the radix fallback
+                kmin = static_cast<K>(~static_cast<K>(0));
+                kmax = 0;
                 for (uint64_t i = pos + tid; i < e; i += BLOCK) {
                     const K k = keys[i];
                     kmin = k < kmin ? k : kmin;
                     kmax = k > kmax ? k : kmax;
                 }
-                uint32_t dummy = 0;
-                block_count_minmax<K, BLOCK>(dummy, kmin, kmax, sm.red);
+                block_minmax2<K, BLOCK>(kmin, kmax, sm.red);
                 if (tid == 0 && kmin != kmax) {
                     atomicAdd(&bst->oversized, 1u);
                     atomicMax(&bst->span_lo_not, ~static_cast<unsigned long long>(pos));
@@ -400,87 +512,15 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             continue;
         }
 
-        // ---- stable in-smem LSD sort of sm.keys[0, ls) by (key - min), r-bit digits
-        // Same rank primitive as the one-sweep pass: per-warp counters pre-scanned into
-        // slot bases, slot = atomicAdd (lane-ordered, program-ordered => stable).
+        // ---- stable in-smem LSD sort of sm.keys[0, ls) by (key - min)
         const int len_s = static_cast<int>(ls);
         const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
-        const int passes = (bits + kWinDigitBits - 1) / kWinDigitBits;
-        const int r = (bits + passes - 1) / passes;
-        const uint32_t nbins = 1u << r, mask = nbins - 1u;
+        const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
         K* ka = sm.keys;
         K* kb = sm.keys2;
         uint32_t* va = sm.vals;
         uint32_t* vb = sm.vals2;
-        const int ipt = (len_s + BLOCK - 1) / BLOCK;  // items per thread sized to this stage
-        const int wofs = warp * 32 * ipt + static_cast<int>(lane);
-        for (int pass = 0; pass < passes; ++pass) {
-            const uint32_t shift = static_cast<uint32_t>(pass * r);
-            for (int i = tid; i < kWarps * static_cast<int>(nbins); i += BLOCK)
-                sm.cnt[i / static_cast<int>(nbins)][i % static_cast<int>(nbins)] = 0;
-            __syncthreads();
-            uint32_t* wc = sm.cnt[warp];
-#pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const int o = wofs + i * 32;
-                if (i < ipt && o < len_s)
-                    atomicAdd(&wc[static_cast<uint32_t>((ka[o] - kmin) >> shift) & mask], 1u);
-            }
-            __syncthreads();
-            // bins [tid*BPT, tid*BPT + BPT): totals over warps, block scan over bins, per-warp bases
-            constexpr int BPT = kWinBins / BLOCK > 0 ? kWinBins / BLOCK : 1;
-            uint32_t btot[BPT], tsum = 0;
-#pragma unroll
-            for (int q = 0; q < BPT; ++q) {
-                const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
-                uint32_t t = 0;
-                if (b < nbins) {
-#pragma unroll 4
-                    for (int w = 0; w < kWarps; ++w) t += sm.cnt[w][b];
-                }
-                btot[q] = t;
-                tsum += t;
-            }
-            const uint32_t inc = warp_inclusive_scan(tsum);
-            if (lane == 31) sm.scan_tot[warp] = inc;
-            __syncthreads();
-            {
-                uint32_t base = inc - tsum;
-                for (int w = 0; w < warp; ++w) base += sm.scan_tot[w];
-#pragma unroll
-                for (int q = 0; q < BPT; ++q) {
-                    const uint32_t b = static_cast<uint32_t>(tid * BPT + q);
-                    if (b < nbins) {
-                        uint32_t bb = base;
-#pragma unroll 4
-                        for (int w = 0; w < kWarps; ++w) {
-                            const uint32_t v = sm.cnt[w][b];
-                            sm.cnt[w][b] = bb;
-                            bb += v;
-                        }
-                    }
-                    base += btot[q];
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const int o = wofs + i * 32;
-                if (i < ipt && o < len_s) {
-                    const K k = ka[o];
-                    const uint32_t slot = atomicAdd(&wc[static_cast<uint32_t>((k - kmin) >> shift) & mask], 1u);
-                    kb[slot] = k;
-                    if (VALS) vb[slot] = va[o];
-                }
-            }
-            __syncthreads();
-            K* tk = ka;
-            ka = kb;
-            kb = tk;
-            uint32_t* tv = va;
-            va = vb;
-            vb = tv;
-        }
+        seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, kb, va, vb, len_s, kmin, passes, (bits + passes - 1) / passes);
         for (int j = tid; j < len_s; j += BLOCK) {
             keys[pos + j] = ka[j];
             if (VALS) vals[pos + j] = va[j];

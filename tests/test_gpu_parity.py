@@ -217,6 +217,28 @@ def test_bucket_oversized_super_buckets(cuda, oracle):
     assert np.array_equal(got_i, want_i)
 
 
+@pytest.mark.parametrize("n", [5000, 8191, 8192, 8193, 20_000, 100_003, 1_000_003])
+def test_bucket_segment_kernel_paths(cuda, oracle, n):
+    """The segment kernel's in-stage choices: sort by bucket + per-bucket
+    insertion (short runs, duplicates inside a bucket), the run-cap fallback to a
+    key sort (long runs of distinct keys), stages cut inside a super-bucket, and
+    tight clusters (many keys per bucket next to empty stretches)."""
+    rng = np.random.default_rng(n)
+    cases = {
+        "narrow": rng.integers(0, 1 << 20, size=n, dtype=np.uint64).astype(np.uint32),
+        "triples": np.repeat(rng.integers(0, 1 << 32, size=(n + 2) // 3, dtype=np.uint64), 3)[:n],
+        "clusters": (rng.integers(0, 50, size=n, dtype=np.uint64) * (1 << 26)
+                     + rng.integers(0, 1 << 12, size=n, dtype=np.uint64)),
+    }
+    cases["triples"] = rng.permutation(cases["triples"]).astype(np.uint32)
+    cases["clusters"] = cases["clusters"].astype(np.uint32)
+    for name, k in cases.items():
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        got_k, got_i = dev_sort(k, "bucket", "iota", range_bound=U32_MAX)
+        assert np.array_equal(got_k, want_k), (name, n)
+        assert np.array_equal(got_i, want_i), (name, n)
+
+
 # ------------------------------------------------------- config-shaped checksums (10^6)
 def test_config_shaped_checksums_match_reference(cuda, oracle):
     with open(os.path.join(GOLDEN, "reference_checksums.json")) as f:
