@@ -171,6 +171,8 @@ struct BucketDigitizer {
     uint32_t s_lo;                     // super-bucket = b >> s_lo
     uint32_t used;                     // number of digit passes that can be non-trivial
 
+    uint32_t tsh[kBucketMaxDigits];    // kPow2Narrow: log2(M + 1) + shift[p], capped at 64 (=> 0)
+
     static BucketDigitizer make(uint64_t n, uint64_t bound) {
         BucketDigitizer d{};
         d.bi = BucketIndexer::make(n, bound);
@@ -179,23 +181,37 @@ struct BucketDigitizer {
         if (db > kBucketMaxDigits) db = kBucketMaxDigits;
         d.used = db;
         d.s_lo = L > 8 * db ? L - 8 * db : 0;
-        for (uint32_t p = 0; p < kBucketMaxDigits; ++p) d.shift[p] = p < db ? d.s_lo + 8 * p : 63;
+        for (uint32_t p = 0; p < kBucketMaxDigits; ++p) {
+            d.shift[p] = p < db ? d.s_lo + 8 * p : 63;
+            const uint32_t t = (d.bi.pow2_shift < 64 ? d.bi.pow2_shift : 64) + d.shift[p];
+            d.tsh[p] = t < 64 ? t : 64;
+        }
         return d;
     }
-    __device__ __forceinline__ uint32_t digit_of_bucket(uint64_t b, int pos) const {
-        return static_cast<uint32_t>(b >> shift_for(pos)) & (kRadix - 1);
-    }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
-        return pos == 0 ? shift[0] : (pos == 1 ? shift[1] : shift[2]);
+        const uint32_t* t = MODE == kPow2Narrow ? tsh : shift;
+        return pos == 0 ? t[0] : (pos == 1 ? t[1] : t[2]);
     }
+    // Digit of the bucket index.  Keys above M only reach here when the call is
+    // failing with a range error; their digits are then meaningless but < 256.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
+        if (MODE == kPow2Narrow) {  // floor(n * key / 2^s) >> shift = (n * key) >> (s + shift); n < 2^32
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+            return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
+        }
         return static_cast<uint32_t>(bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
     }
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
+        if (MODE == kPow2Narrow) {
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+#pragma unroll
+            for (int q = 0; q < kDigits; ++q) d[q] = tsh[q] < 64 ? static_cast<uint32_t>(p >> tsh[q]) & (kRadix - 1) : 0u;
+            return;
+        }
         const uint64_t b = bucket_of<MODE>(bi, static_cast<uint64_t>(key));
 #pragma unroll
-        for (int p = 0; p < kDigits; ++p) d[p] = static_cast<uint32_t>(b >> shift[p]) & (kRadix - 1);
+        for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const { return static_cast<uint64_t>(key) <= bi.bound; }
     __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }
