@@ -260,7 +260,8 @@ struct OnesweepSmem {
     uint32_t tile_id;
 };
 
-constexpr int kLookbackWindow = 16;  // predecessors read per round trip, per digit
+constexpr int kLookbackWindow = 16;
+constexpr int kHotDigits = 32;  // <= this many distinct digits in a tile: warp-aggregated atomics  // predecessors read per round trip, per digit
 
 // Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back,
 // all kLookbackWindow loads in flight per round trip.
@@ -341,8 +342,40 @@ __device__ __forceinline__ uint32_t warp_slot(uint32_t* wc, uint32_t d) {
     return atomicAdd(&wc[d], 1u);
 }
 
+// Tiles made of sorted runs (sorted or reverse-sorted input, the bucket sort's
+// high digits): when the whole warp shares the digit, one atomic of 32 replaces
+// 32 same-address atomics (which serialise).  Full warps only; lane order is
+// kept, so the slot stays stable.  `agg` is warp-uniform: it switches off at the
+// first mixed instruction, so random tiles pay one vote per warp and chunk.
+template <bool SAFE>
+__device__ __forceinline__ uint32_t warp_slot_agg(uint32_t* wc, uint32_t d, bool& agg) {
+    if (agg) {
+        const uint32_t d0 = __shfl_sync(ISORT_FULL_MASK, d, 0);
+        if (__all_sync(ISORT_FULL_MASK, d == d0)) {
+            uint32_t old = 0;
+            if (lane_id() == 0) old = atomicAdd(&wc[d0], 32u);
+            return __shfl_sync(ISORT_FULL_MASK, old, 0) + lane_id();
+        }
+        agg = false;
+    }
+    return warp_slot<SAFE>(wc, d);
+}
+
+template <bool AGG>
+__device__ __forceinline__ void count_digit_t(uint32_t* wc, uint32_t d, bool& agg) {
+    if (AGG && agg) {
+        const uint32_t d0 = __shfl_sync(ISORT_FULL_MASK, d, 0);
+        if (__all_sync(ISORT_FULL_MASK, d == d0)) {
+            if (lane_id() == 0) atomicAdd(&wc[d0], 32u);
+            return;
+        }
+        agg = false;
+    }
+    atomicAdd(&wc[d], 1u);
+}
+
 // Phase 2 for one chunk.  FULL: all BLOCK*IPT keys valid (no bounds checks).
-template <bool FULL, bool SAFE, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
+template <bool FULL, bool AGG, bool SAFE, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
 __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restrict__ csrc,
                                                const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                                                K* __restrict__ dst, uint64_t cbase, uint32_t valid, bool gen_iota,
@@ -362,11 +395,12 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
                               : ((FULL || wofs + i * 32u < valid) ? ldg_stream(vsrc + cbase + wofs + i * 32u) : 0u);
     }
     uint32_t* wc = sm.cnt[c][warp];
+    bool agg = FULL && AGG;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         if (FULL || wofs + i * 32u < valid) {
             const uint32_t d = dz.digit_sh(key[i], dsh);
-            const uint32_t s = warp_slot<SAFE>(wc, d);
+            const uint32_t s = (FULL && AGG) ? warp_slot_agg<SAFE>(wc, d, agg) : warp_slot<SAFE>(wc, d);
             sm.keys[s] = key[i];
             if (VALS) sm.vals[s] = val[i];
             if (!Dz::kCheapDigit) sm.digits[s] = static_cast<uint8_t>(d);
@@ -386,6 +420,70 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
         }
     }
     __syncthreads();
+}
+
+// Phase 1: per-(chunk, warp) digit counts of one tile (keys via L2, kept there
+// for phase 2).  AGG: the tile is expected to be made of sorted runs.
+template <bool AGG, typename K, typename Dz, int IPT, int NCHUNK, typename Smem>
+__device__ __forceinline__ void onesweep_count(Smem& sm, const K* __restrict__ src, uint64_t tile_base,
+                                               uint32_t tile_len, int warp, uint32_t lane, bool vec, const Dz& dz,
+                                               uint32_t dsh, uint64_t pol_keep) {
+    constexpr int kChunk = Smem::kChunk;
+#pragma unroll 1
+    for (int c = 0; c < NCHUNK; c += (NCHUNK >= 2 ? 2 : 1)) {
+        const uint32_t c0 = static_cast<uint32_t>(c) * kChunk + static_cast<uint32_t>(warp) * 32u * IPT;
+        const uint32_t c1 = c0 + kChunk;
+        uint32_t* wc0 = sm.cnt[c][warp];
+        uint32_t* wc1 = sm.cnt[NCHUNK >= 2 ? c + 1 : c][warp];
+        const K* ws = src + tile_base + c0;
+        bool agg1 = AGG;
+        if (NCHUNK == 1) {
+            if (vec && c0 + 32u * IPT <= tile_len) {
+                const uint4* v0 = reinterpret_cast<const uint4*>(ws);
+                uint4 x[IPT / 4 > 0 ? IPT / 4 : 1];
+#pragma unroll
+                for (int q = 0; q < IPT / 4; ++q) x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
+#pragma unroll
+                for (int q = 0; q < IPT / 4; ++q) {
+                    count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].x), dsh), agg1);
+                    count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].y), dsh), agg1);
+                    count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].z), dsh), agg1);
+                    count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].w), dsh), agg1);
+                }
+            } else {
+                for (uint32_t o = lane; o < 32u * IPT; o += 32)
+                    if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
+            }
+            continue;
+        }
+        if (vec && c1 + 32u * IPT <= tile_len) {
+            const uint4* v0 = reinterpret_cast<const uint4*>(ws);
+            const uint4* v1 = reinterpret_cast<const uint4*>(ws + kChunk);
+            uint4 x[IPT / 4 > 0 ? IPT / 4 : 1], y[IPT / 4 > 0 ? IPT / 4 : 1];
+#pragma unroll
+            for (int q = 0; q < IPT / 4; ++q) {
+                x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
+                y[q] = ldg_v4_hint(v1 + lane + 32 * q, pol_keep);
+            }
+#pragma unroll
+            for (int q = 0; q < IPT / 4; ++q) {
+                count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].x), dsh), agg1);
+                count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].y), dsh), agg1);
+                count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].z), dsh), agg1);
+                count_digit_t<AGG>(wc0, dz.digit_sh(static_cast<K>(x[q].w), dsh), agg1);
+                count_digit_t<AGG>(wc1, dz.digit_sh(static_cast<K>(y[q].x), dsh), agg1);
+                count_digit_t<AGG>(wc1, dz.digit_sh(static_cast<K>(y[q].y), dsh), agg1);
+                count_digit_t<AGG>(wc1, dz.digit_sh(static_cast<K>(y[q].z), dsh), agg1);
+                count_digit_t<AGG>(wc1, dz.digit_sh(static_cast<K>(y[q].w), dsh), agg1);
+            }
+        } else {
+            for (uint32_t o = lane; o < 32u * IPT; o += 32) {
+                if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
+                if (c1 + o < tile_len)
+                    atomicAdd(&wc1[dz.digit_sh(ldg_hint(ws + kChunk + o, pol_keep), dsh)], 1u);
+            }
+        }
+    }
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE>
@@ -432,6 +530,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 #define ISORT_TICK(v)
 #endif
 
+    bool hot_prev = false;  // phase 1 guesses from this CTA's previous tile
     for (;;) {
         ISORT_TICK(q0);
         if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
@@ -447,64 +546,15 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                                                             ? n - tile_base : static_cast<uint64_t>(kTile));
 
         // ---------------- phase 1: per-(chunk, warp) digit counts
-#pragma unroll 1
-        for (int c = 0; c < NCHUNK; c += (NCHUNK >= 2 ? 2 : 1)) {
-            const uint32_t c0 = static_cast<uint32_t>(c) * kChunk + static_cast<uint32_t>(warp) * 32u * IPT;
-            const uint32_t c1 = c0 + kChunk;
-            uint32_t* wc0 = sm.cnt[c][warp];
-            uint32_t* wc1 = sm.cnt[NCHUNK >= 2 ? c + 1 : c][warp];
-            const K* ws = src + tile_base + c0;
-            if (NCHUNK == 1) {
-                if (vec && c0 + 32u * IPT <= tile_len) {
-                    const uint4* v0 = reinterpret_cast<const uint4*>(ws);
-                    uint4 x[IPT / 4 > 0 ? IPT / 4 : 1];
-#pragma unroll
-                    for (int q = 0; q < IPT / 4; ++q) x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
-#pragma unroll
-                    for (int q = 0; q < IPT / 4; ++q) {
-                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].x), dsh)], 1u);
-                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].y), dsh)], 1u);
-                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].z), dsh)], 1u);
-                        atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].w), dsh)], 1u);
-                    }
-                } else {
-                    for (uint32_t o = lane; o < 32u * IPT; o += 32)
-                        if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
-                }
-                continue;
-            }
-            if (vec && c1 + 32u * IPT <= tile_len) {
-                const uint4* v0 = reinterpret_cast<const uint4*>(ws);
-                const uint4* v1 = reinterpret_cast<const uint4*>(ws + kChunk);
-                uint4 x[IPT / 4 > 0 ? IPT / 4 : 1], y[IPT / 4 > 0 ? IPT / 4 : 1];
-#pragma unroll
-                for (int q = 0; q < IPT / 4; ++q) {
-                    x[q] = ldg_v4_hint(v0 + lane + 32 * q, pol_keep);
-                    y[q] = ldg_v4_hint(v1 + lane + 32 * q, pol_keep);
-                }
-#pragma unroll
-                for (int q = 0; q < IPT / 4; ++q) {
-                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].x), dsh)], 1u);
-                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].y), dsh)], 1u);
-                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].z), dsh)], 1u);
-                    atomicAdd(&wc0[dz.digit_sh(static_cast<K>(x[q].w), dsh)], 1u);
-                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].x), dsh)], 1u);
-                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].y), dsh)], 1u);
-                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].z), dsh)], 1u);
-                    atomicAdd(&wc1[dz.digit_sh(static_cast<K>(y[q].w), dsh)], 1u);
-                }
-            } else {
-                for (uint32_t o = lane; o < 32u * IPT; o += 32) {
-                    if (c0 + o < tile_len) atomicAdd(&wc0[dz.digit_sh(ldg_hint(ws + o, pol_keep), dsh)], 1u);
-                    if (c1 + o < tile_len)
-                        atomicAdd(&wc1[dz.digit_sh(ldg_hint(ws + kChunk + o, pol_keep), dsh)], 1u);
-                }
-            }
-        }
+        if (hot_prev)
+            onesweep_count<true, K, Dz, IPT, NCHUNK>(sm, src, tile_base, tile_len, warp, lane, vec, dz, dsh, pol_keep);
+        else
+            onesweep_count<false, K, Dz, IPT, NCHUNK>(sm, src, tile_base, tile_len, warp, lane, vec, dz, dsh, pol_keep);
         __syncthreads();
         ISORT_TICK(q1);
 
         // ---------------- one thread per digit: totals, look-back, slot bases
+        int nonzero = 0;
         if (tid < kRadix) {
             const int d = tid;
             uint32_t cc[NCHUNK], tot = 0;
@@ -516,6 +566,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 cc[c] = x;
                 tot += x;
             }
+            nonzero = tot != 0;
             uint32_t excl = 0;
             if (tile == 0) {
                 st_relaxed_gpu(&lb[d], kFlagInc | tot);
@@ -552,7 +603,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 }
             }
         }
-        __syncthreads();
+        // A tile with few distinct digits comes from sorted runs (sorted or
+        // reverse-sorted input, or the bucket sort's high digits): warps mostly
+        // share one digit, so rank/count them with one atomic per warp.
+        const bool hot = __syncthreads_count(nonzero) <= kHotDigits;
+        hot_prev = hot;
 
         // ---------------- phase 2: stage by slot, coalesced scatter
 #pragma unroll 1
@@ -561,12 +616,18 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             if (c0 >= tile_len) break;
             const uint32_t valid = tile_len - c0 < static_cast<uint32_t>(kChunk) ? tile_len - c0 : kChunk;
             const uint64_t cbase = tile_base + c0;
-            if (valid == static_cast<uint32_t>(kChunk))
-                onesweep_chunk<true, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase, valid,
-                                                                    gen_iota, dsh, dz, warp, lane, pol_stream);
+            if (valid == static_cast<uint32_t>(kChunk) && hot)
+                onesweep_chunk<true, true, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                                                                          valid, gen_iota, dsh, dz, warp, lane,
+                                                                          pol_stream);
+            else if (valid == static_cast<uint32_t>(kChunk))
+                onesweep_chunk<true, false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                                                                           valid, gen_iota, dsh, dz, warp, lane,
+                                                                           pol_stream);
             else
-                onesweep_chunk<false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
-                                                                     valid, gen_iota, dsh, dz, warp, lane, pol_stream);
+                onesweep_chunk<false, false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                                                                            valid, gen_iota, dsh, dz, warp, lane,
+                                                                            pol_stream);
         }
         ISORT_TICK(q3);
 #ifdef ISORT_PHASE_TIMING
