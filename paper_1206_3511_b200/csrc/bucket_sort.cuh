@@ -236,16 +236,93 @@ constexpr int kSegWords = 1 << (kSegDigitBits - 1);
 
 template <typename K, int BLOCK, int IPT, bool VALS>
 struct SegSmem {
-    K keys[BLOCK * IPT];
-    K keys2[BLOCK * IPT];  // ping-pong buffer of the in-smem sort
-    uint32_t vals[VALS ? BLOCK * IPT : 1];
-    uint32_t vals2[VALS ? BLOCK * IPT : 1];
+    static constexpr int kCap = BLOCK * IPT + 4;  // a stage + slack that keeps bulk copies 16-byte aligned
+    alignas(16) K buf[2][kCap];                   // incoming stage / in-smem sort ping-pong
+    alignas(16) uint32_t vbuf[2][VALS ? kCap : 1];
     alignas(16) uint32_t cnt[BLOCK / 32][kSegWords];  // per-warp packed digit counters, then slot bases
     uint32_t scan_tot[BLOCK / 32];
     unsigned long long red[2][BLOCK / 32];
     unsigned long long pos[2];  // segment bounds, then the end of an oversized super-bucket
-    int ls;                     // start of the stage's last super-bucket
+    alignas(8) unsigned long long bar;  // mbarrier: bulk stage load landed
+    int ls;                             // start of the stage's last super-bucket
 };
+
+// ---- bulk (TMA) global -> shared copies completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+// Orders this thread's generic-proxy shared accesses before later async-proxy ones.
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Split of src[pos, pos + len) into a head (up to the first 16-byte boundary),
+// a bulk-copyable interior of whole 16-byte blocks, and a tail.  Element j is
+// staged at dst[off + j], which puts the interior on a 16-byte boundary.
+struct BulkSplit {
+    int off, head, body;  // body: interior elements
+};
+template <typename T>
+__device__ __forceinline__ BulkSplit bulk_split(const T* src, uint64_t pos, int len) {
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src + pos) & 15u);
+    BulkSplit b;
+    b.off = static_cast<int>(mis / sizeof(T));
+    const int h = static_cast<int>(((16u - mis) & 15u) / sizeof(T));
+    b.head = h < len ? h : len;
+    b.body = ((len - b.head) * static_cast<int>(sizeof(T)) / 16) * 16 / static_cast<int>(sizeof(T));
+    return b;
+}
+
+// Start loading stage [pos, pos + len) of keys (and payload) into kd / vd: the
+// interiors by bulk copies on `bar` (thread 0), heads and tails by plain loads.
+// Call with the whole CTA after a barrier that freed kd / vd.
+template <typename K, bool VALS>
+__device__ __forceinline__ void seg_issue(const K* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t pos,
+                                          int len, K* kd, uint32_t* vd, unsigned long long* bar, BulkSplit& kb,
+                                          BulkSplit& vb) {
+    kb = bulk_split(keys, pos, len);
+    if (VALS) vb = bulk_split(vals, pos, len);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_expect_tx(bar, static_cast<uint32_t>(kb.body * sizeof(K) + (VALS ? vb.body * 4 : 0)));
+        if (kb.body) bulk_g2s(kd + kb.off + kb.head, keys + pos + kb.head, kb.body * sizeof(K), bar);
+        if (VALS && vb.body) bulk_g2s(vd + vb.off + vb.head, vals + pos + vb.head, vb.body * 4u, bar);
+    }
+    const int kplain = len - kb.body;  // head + tail elements
+    if (tid < kplain) {
+        const int j = tid < kb.head ? tid : kb.body + tid;
+        kd[kb.off + j] = keys[pos + j];
+    }
+    if (VALS) {
+        const int vplain = len - vb.body;
+        if (tid >= 32 && tid - 32 < vplain) {
+            const int t = tid - 32;
+            const int j = t < vb.head ? t : vb.body + t;
+            vd[vb.off + j] = vals[pos + j];
+        }
+    }
+}
 
 // First index in [lo, hi) where the monotone predicate holds, or hi.  Called by a
 // whole warp: 32 probes per round narrow the range 32x.
@@ -315,32 +392,6 @@ __device__ __forceinline__ void seg_rank(K* kb, const uint32_t* va, uint32_t* vb
             const uint32_t slot = (atomicAdd(&wc[d >> 1], 1u << h) >> h) & 0xFFFFu;
             kb[slot] = kv[i];
             if (VALS) vb[slot] = va[o];
-        }
-    }
-}
-
-// Stage keys[pos, pos + len) (and payload) into shared memory; min/max of the keys.
-template <bool FULL, typename K, int BLOCK, int IPT, bool VALS>
-__device__ __forceinline__ void seg_stage(const K* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t pos,
-                                          int len, K* skeys, uint32_t* svals, K& kmin, K& kmax) {
-    K kr[IPT];
-    uint32_t vr[VALS ? IPT : 1];
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int j = static_cast<int>(threadIdx.x) + i * BLOCK;
-        if (FULL || j < len) {
-            kr[i] = keys[pos + j];
-            if (VALS) vr[i] = vals[pos + j];
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int j = static_cast<int>(threadIdx.x) + i * BLOCK;
-        if (FULL || j < len) {
-            skeys[j] = kr[i];
-            if (VALS) svals[j] = vr[i];
-            kmin = kr[i] < kmin ? kr[i] : kmin;
-            kmax = kr[i] > kmax ? kr[i] : kmax;
         }
     }
 }
@@ -465,29 +516,47 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         const uint64_t p = warp_next_start(keys, n, x, dz);
         if (lane == 0) sm.pos[warp] = p;
     }
+    if (tid == 0) mbar_init(&sm.bar, 1);
     __syncthreads();
     uint64_t pos = sm.pos[0];
     const uint64_t seg_hi = sm.pos[1];
+    auto stage_len = [&](uint64_t p) {
+        return seg_hi - p < static_cast<uint64_t>(kStage) ? static_cast<int>(seg_hi - p) : kStage;
+    };
 
+    // Stage i+1 streams in (bulk copy) while stage i is written back.
+    int cur = 0;
+    uint32_t phase = 0;
+    BulkSplit ksp{}, vsp{};
+    if (pos < seg_hi) seg_issue<K, VALS>(keys, vals, pos, stage_len(pos), sm.buf[cur], sm.vbuf[cur], &sm.bar, ksp, vsp);
+    __syncthreads();
     while (pos < seg_hi) {
-        const int len = seg_hi - pos < static_cast<uint64_t>(kStage) ? static_cast<int>(seg_hi - pos) : kStage;
+        const int len = stage_len(pos);
         const bool tail = pos + len == seg_hi;  // ends on a super-bucket start: all complete
-        // ---- stage; min/max of the stage (a superset of the sorted part is fine:
-        // the tail super-bucket's keys are all larger than the complete ones')
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
+        K* ka = sm.buf[cur] + ksp.off;
+        uint32_t* va = VALS ? sm.vbuf[cur] + vsp.off : nullptr;
+        // ---- min/max of the stage (a superset of the sorted part is fine: the
+        // tail super-bucket's keys are all larger than the complete ones')
         K kmin = static_cast<K>(~static_cast<K>(0)), kmax = 0;
-        if (len == kStage)
-            seg_stage<true, K, BLOCK, IPT, VALS>(keys, vals, pos, len, sm.keys, sm.vals, kmin, kmax);
-        else
-            seg_stage<false, K, BLOCK, IPT, VALS>(keys, vals, pos, len, sm.keys, sm.vals, kmin, kmax);
-        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int j = tid + i * BLOCK;
+            if (j < len) {
+                const K k = ka[j];
+                kmin = k < kmin ? k : kmin;
+                kmax = k > kmax ? k : kmax;
+            }
+        }
         // ---- ls = start of the last (possibly incomplete) super-bucket: a lower bound
         // over the staged keys, which are ordered by super-bucket
         if (warp == 0) {
             int l = len;
             if (!tail) {
-                const uint64_t sbl = dz.super_bucket(sm.keys[len - 1]);
+                const uint64_t sbl = dz.super_bucket(ka[len - 1]);
                 l = static_cast<int>(warp_first_true(0, static_cast<uint64_t>(len), [&](uint64_t j) {
-                    return dz.super_bucket(sm.keys[j]) == sbl;
+                    return dz.super_bucket(ka[j]) == sbl;
                 }));
             }
             if (lane == 0) sm.ls = l;
@@ -504,6 +573,10 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             if (e == pos + static_cast<uint64_t>(len)) {  // ends exactly with the stage
                 ls = len;
             } else {  // oversized: constant (nothing to do) or a span for the radix fallback
+                fence_proxy_async_smem();
+                __syncthreads();
+                cur ^= 1;
+                if (e < seg_hi) seg_issue<K, VALS>(keys, vals, e, stage_len(e), sm.buf[cur], sm.vbuf[cur], &sm.bar, ksp, vsp);
                 kmin = static_cast<K>(~static_cast<K>(0));
                 kmax = 0;
                 for (uint64_t i = pos + tid; i < e; i += BLOCK) {
@@ -522,26 +595,36 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 continue;
             }
         }
+        const uint64_t next = pos + static_cast<uint64_t>(ls);
         if (kmin == kmax) {  // one key value (or one key): arrival order is the answer, in place
-            pos += ls;
+            fence_proxy_async_smem();
+            __syncthreads();
+            cur ^= 1;
+            if (next < seg_hi)
+                seg_issue<K, VALS>(keys, vals, next, stage_len(next), sm.buf[cur], sm.vbuf[cur], &sm.bar, ksp, vsp);
+            pos = next;
             __syncthreads();
             continue;
         }
 
-        // ---- stable in-smem LSD sort of sm.keys[0, ls) by (key - min)
-        const int len_s = static_cast<int>(ls);
+        // ---- stable in-smem LSD sort of ka[0, ls) by (key - min), ping-pong with the other buffer
         const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
         const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
-        K* ka = sm.keys;
-        K* kb = sm.keys2;
-        uint32_t* va = sm.vals;
-        uint32_t* vb = sm.vals2;
-        seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, kb, va, vb, len_s, kmin, passes, (bits + passes - 1) / passes);
-        for (int j = tid; j < len_s; j += BLOCK) {
+        K* kb = sm.buf[cur ^ 1];
+        uint32_t* vb = VALS ? sm.vbuf[cur ^ 1] : nullptr;
+        seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, kb, va, vb, ls, kmin, passes, (bits + passes - 1) / passes);
+        // the result is in ka; the next stage goes to the other buffer
+        const int tgt = ka == sm.buf[cur] + ksp.off ? cur ^ 1 : cur;
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (next < seg_hi)
+            seg_issue<K, VALS>(keys, vals, next, stage_len(next), sm.buf[tgt], sm.vbuf[tgt], &sm.bar, ksp, vsp);
+        for (int j = tid; j < ls; j += BLOCK) {
             keys[pos + j] = ka[j];
             if (VALS) vals[pos + j] = va[j];
         }
-        pos += ls;
+        cur = tgt;
+        pos = next;
         __syncthreads();
     }
 }
