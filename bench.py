@@ -41,6 +41,17 @@ N_DEFAULT = 100_000_000
 FALLBACK_HBM_GBS = 6650.0
 
 
+def ncu_traffic(family):
+    """Per-launch DRAM bytes of a kernel family from a committed `ncu --set full`
+    capture (tools/ncu_traffic.py -> profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)[family]
+        return t["dram_bytes_per_launch"], t["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -331,10 +342,12 @@ def main_ours(args):
         if world == 1:
             pass_bytes = 8 * n  # read 4n + write 4n per one-sweep pass (keys only)
             achieved = pass_bytes / (r["pass_ms"] / 1e3) / 1e9 if r["pass_ms"] else None
+            traffic, traffic_src = ncu_traffic("k_onesweep") if n == N_DEFAULT else (None, None)
             line["roofline"] = {
                 "bound": "hbm", "kernel": "k_onesweep<u32> (one digit pass)", "achieved": achieved,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None, "traffic": None,
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": pass_bytes, "launch_ms": r["pass_ms"],
                 "passes_executed": r["n_active"],
                 "whole_sort_bytes": 4 * n + 8 * n * r["n_active"],
@@ -344,8 +357,16 @@ def main_ours(args):
             line["gpu_launches"] = r["launches"]
             line["clocks"] = r["clocks"]
             line["parity"] = {"radix": r["parity"], "bucket": b["parity"]}
-            bb = 4 * n + 8 * n * b["n_active"] + 8 * n  # hist + passes + window sort
+            bb = 4 * n + 8 * n * b["n_active"] + 8 * n  # hist + passes + segment sort
+            seg_ms = b["phases"].get("segments")
+            seg_traffic, seg_src = ncu_traffic("k_bucket_segments") if n == N_DEFAULT else (None, None)
+            seg_ach = 8 * n / (seg_ms / 1e3) / 1e9 if seg_ms else None
             line["bucket"] = {"value": bvalue, "ms_per_step": b["ms"], "passes_executed": b["n_active"],
+                              "roofline": {"bound": "hbm", "kernel": "k_bucket_segments<u32> (in-smem sort of "
+                                           "the super-buckets, in place)", "achieved": seg_ach, "peak": peak,
+                                           "unit": "GB/s", "frac": seg_ach / peak if seg_ach else None,
+                                           "traffic": seg_traffic, "traffic_source": seg_src,
+                                           "algorithmic_bytes_per_launch": 8 * n, "launch_ms": seg_ms},
                               "phases_ms": {k: round(v, 4) for k, v in b["phases"].items()},
                               "whole_sort_bytes": bb, "whole_sort_frac": bb / (b["ms"] / 1e3) / 1e9 / peak,
                               "gpu_launches": b["launches"]}
