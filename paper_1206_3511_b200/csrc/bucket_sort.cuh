@@ -172,6 +172,9 @@ struct BucketDigitizer {
     uint32_t used;                     // number of digit passes that can be non-trivial
 
     uint32_t tsh[kBucketMaxDigits];    // kPow2Narrow: log2(M + 1) + shift[p], capped at 64 (=> 0)
+    uint32_t tshc[kBucketMaxDigits];   // min(tsh, 63) with dmask = 0 when tsh == 64: branch-free digits
+    uint32_t dmask[kBucketMaxDigits];
+    uint32_t check_range;              // M < the largest key value: keys can be out of range
 
     static BucketDigitizer make(uint64_t n, uint64_t bound) {
         BucketDigitizer d{};
@@ -185,7 +188,10 @@ struct BucketDigitizer {
             d.shift[p] = p < db ? d.s_lo + 8 * p : 63;
             const uint32_t t = (d.bi.pow2_shift < 64 ? d.bi.pow2_shift : 64) + d.shift[p];
             d.tsh[p] = t < 64 ? t : 64;
+            d.tshc[p] = t < 64 ? t : 63;
+            d.dmask[p] = t < 64 ? kRadix - 1 : 0;
         }
+        d.check_range = bound < static_cast<uint64_t>(~static_cast<K>(0)) ? 1u : 0u;
         return d;
     }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
@@ -206,14 +212,16 @@ struct BucketDigitizer {
         if (MODE == kPow2Narrow) {
             const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
 #pragma unroll
-            for (int q = 0; q < kDigits; ++q) d[q] = tsh[q] < 64 ? static_cast<uint32_t>(p >> tsh[q]) & (kRadix - 1) : 0u;
+            for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;
         }
         const uint64_t b = bucket_of<MODE>(bi, static_cast<uint64_t>(key));
 #pragma unroll
         for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
-    __device__ __forceinline__ bool in_range(K key) const { return static_cast<uint64_t>(key) <= bi.bound; }
+    __device__ __forceinline__ bool in_range(K key) const {
+        return !check_range || static_cast<uint64_t>(key) <= bi.bound;
+    }
     __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }
     __device__ __forceinline__ uint64_t super_bucket(K key) const {
         return bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> s_lo;

@@ -87,7 +87,10 @@ constexpr uint64_t kSmallN = 4ull << 20;
 template <typename K, bool VALS, int CHUNKS = 4>
 struct PassCfg {
     static constexpr int kBlock = ISORT_PASS_BLOCK;
-    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : 12) : (VALS ? 6 : 8);
+#ifndef ISORT_PASS_IPT32
+#define ISORT_PASS_IPT32 12
+#endif
+    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : ISORT_PASS_IPT32) : (VALS ? 6 : 8);
     static constexpr int kChunks = CHUNKS;
     static constexpr int kTile = kBlock * kIpt * kChunks;
     static constexpr int kCtasPerSm = 1024 / kBlock;
@@ -100,8 +103,14 @@ inline int pass_tile(uint64_t n) {
 
 // Upfront histogram replication (lane copies per bin): 64 KB of counters.
 template <int D>
+#ifndef ISORT_UF_REP
+#define ISORT_UF_REP 16
+#endif
+#ifndef ISORT_UF_BLOCK
+#define ISORT_UF_BLOCK 512
+#endif
 struct UpfrontCfg {
-    static constexpr int kRep = D <= 4 ? 16 : 8;
+    static constexpr int kRep = D <= 4 ? ISORT_UF_REP : 8;
     static constexpr size_t kSmem = static_cast<size_t>(D) * kRadix * kRep * sizeof(uint32_t);
 };
 
@@ -134,7 +143,7 @@ bool rank_fast_path_ok() {
     return bad == 0;
 }
 
-constexpr int kUpfrontBlock = 512;
+constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
 struct RadixLayout {
     size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
@@ -181,6 +190,24 @@ void set_max_smem_once(F* kernel, size_t bytes) {
     g_smem_done.insert(key);
 }
 
+// CTAs of `kernel` resident per SM (occupancy API), once per (kernel, device).
+std::map<std::pair<const void*, int>, int> g_occ;
+
+template <typename F>
+int resident_per_sm(F* kernel, int block, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    std::lock_guard<std::mutex> g(g_smem_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    if (per_sm < 1) per_sm = 1;
+    g_occ[key] = per_sm;
+    return per_sm;
+}
+
 template <typename K, bool VALS, typename Dz, typename Cfg>
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
                    uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s) {
@@ -220,16 +247,11 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     const bool vec = (reinterpret_cast<uintptr_t>(kin) & 15u) == 0;
     using UCfg = UpfrontCfg<D>;
     const uint64_t want = (n + 4ull * kUpfrontBlock - 1) / (4ull * kUpfrontBlock);
-    const unsigned grid1 = static_cast<unsigned>(want < 3ull * kNumSMs ? (want ? want : 1) : 3ull * kNumSMs);
-    if (vec) {
-        auto* k1 = k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, true>;
-        set_max_smem_once(k1, UCfg::kSmem);
-        k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
-    } else {
-        auto* k1 = k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, false>;
-        set_max_smem_once(k1, UCfg::kSmem);
-        k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
-    }
+    auto* k1 = vec ? k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, true> : k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, false>;
+    set_max_smem_once(k1, UCfg::kSmem);
+    const uint64_t cap1 = static_cast<uint64_t>(resident_per_sm(k1, kUpfrontBlock, UCfg::kSmem)) * kNumSMs;
+    const unsigned grid1 = static_cast<unsigned>(want < cap1 ? (want ? want : 1) : cap1);
+    k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
     prof_mark(s, "upfront");
     k_plan<D><<<1, kRadix, 0, s>>>(st, n, skip_sorted ? 1 : 0);
     prof_mark(s, "plan");
@@ -461,12 +483,7 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
     using Smem = SegSmem<K, kSegBlock, kSegIpt, VALS>;
     auto* kern = k_bucket_segments<K, Dz, kSegBlock, kSegIpt, VALS>;
     set_max_smem_once(kern, sizeof(Smem));
-    static thread_local std::map<const void*, int> occ;
-    int& per_sm = occ[reinterpret_cast<const void*>(kern)];
-    if (per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSegBlock, sizeof(Smem));
-        if (per_sm < 1) per_sm = 1;
-    }
+    const int per_sm = resident_per_sm(kern, kSegBlock, sizeof(Smem));
     const uint64_t want = (n + 4095) / 4096;
     const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
     kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);

@@ -75,6 +75,9 @@ struct RadixDigitizer {
 };
 
 // ------------------------------------------------------------------- K1
+#ifndef ISORT_UF_UNROLL
+#define ISORT_UF_UNROLL 4
+#endif
 // Digit histograms in lane-replicated shared counters: copy (lane % R) of bin b
 // of digit p lives at ((p * 256 + b) * R + lane % R), so lanes of one atomic
 // instruction hit distinct banks (R = 32) or at most 2-way (R = 16).
@@ -110,28 +113,51 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * BLOCK;
     constexpr int V = 4;  // 4 keys per thread-iteration
     if (VEC) {
+        // Each warp streams U consecutive 512-byte blocks per step (U loads in
+        // flight per thread); the successor key for the sortedness check comes
+        // from the next lane, or the next block's lane 0.
         const uint64_t nv = n / V;
-        for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * BLOCK + threadIdx.x; v < nv; v += stride) {
-            K k[V];
-            if (sizeof(K) == 4) {
-                const uint4 q = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + v);
-                k[0] = static_cast<K>(q.x);
-                k[1] = static_cast<K>(q.y);
-                k[2] = static_cast<K>(q.z);
-                k[3] = static_cast<K>(q.w);
-            } else {
-                const uint4 a = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v);
-                const uint4 b = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v + 1);
-                k[0] = static_cast<K>((static_cast<uint64_t>(a.y) << 32) | a.x);
-                k[1] = static_cast<K>((static_cast<uint64_t>(a.w) << 32) | a.z);
-                k[2] = static_cast<K>((static_cast<uint64_t>(b.y) << 32) | b.x);
-                k[3] = static_cast<K>((static_cast<uint64_t>(b.w) << 32) | b.z);
-            }
-            const uint64_t i0 = v * V;
-            const K next = (i0 + V < n) ? keys[i0 + V] : static_cast<K>(~static_cast<K>(0));
-            desc += (k[0] > k[1]) + (k[1] > k[2]) + (k[2] > k[3]) + (k[3] > next);
+        constexpr int U = ISORT_UF_UNROLL;
+        const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (BLOCK / 32) * 32 * U;
+        for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * (BLOCK / 32) + (threadIdx.x >> 5)) * 32 * U; wb < nv;
+             wb += wstride) {
+            K k[U][V];
 #pragma unroll
-            for (int j = 0; j < V; ++j) visit(k[j], i0 + j);
+            for (int u = 0; u < U; ++u) {
+                const uint64_t v = wb + static_cast<uint64_t>(u) * 32 + lane_id();
+                if (v < nv) {
+                    if (sizeof(K) == 4) {
+                        const uint4 q = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + v);
+                        k[u][0] = static_cast<K>(q.x);
+                        k[u][1] = static_cast<K>(q.y);
+                        k[u][2] = static_cast<K>(q.z);
+                        k[u][3] = static_cast<K>(q.w);
+                    } else {
+                        const uint4 a = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v);
+                        const uint4 b = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v + 1);
+                        k[u][0] = static_cast<K>((static_cast<uint64_t>(a.y) << 32) | a.x);
+                        k[u][1] = static_cast<K>((static_cast<uint64_t>(a.w) << 32) | a.z);
+                        k[u][2] = static_cast<K>((static_cast<uint64_t>(b.y) << 32) | b.x);
+                        k[u][3] = static_cast<K>((static_cast<uint64_t>(b.w) << 32) | b.z);
+                    }
+                } else {
+                    k[u][0] = 0;  // keep the shuffles below defined
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t v = wb + static_cast<uint64_t>(u) * 32 + lane_id();
+                K next = __shfl_down_sync(ISORT_FULL_MASK, k[u][0], 1);
+                const K first_next_block = __shfl_sync(ISORT_FULL_MASK, k[u + 1 < U ? u + 1 : u][0], 0);
+                if (lane_id() == 31) next = first_next_block;
+                const bool from_mem = v + 1 >= nv || (lane_id() == 31 && u + 1 == U);
+                if (v < nv) {
+                    if (from_mem) next = (v * V + V < n) ? keys[v * V + V] : static_cast<K>(~static_cast<K>(0));
+                    desc += (k[u][0] > k[u][1]) + (k[u][1] > k[u][2]) + (k[u][2] > k[u][3]) + (k[u][3] > next);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) visit(k[u][j], v * V + j);
+                }
+            }
         }
         for (uint64_t i = nv * V + static_cast<uint64_t>(blockIdx.x) * BLOCK + threadIdx.x; i < n; i += stride) {
             const K k = keys[i];
@@ -260,8 +286,11 @@ struct OnesweepSmem {
     uint32_t tile_id;
 };
 
-constexpr int kLookbackWindow = 16;
-constexpr int kHotDigits = 32;  // <= this many distinct digits in a tile: warp-aggregated atomics  // predecessors read per round trip, per digit
+#ifndef ISORT_LB_WINDOW
+#define ISORT_LB_WINDOW 16
+#endif
+constexpr int kLookbackWindow = ISORT_LB_WINDOW;  // predecessors read per round trip, per digit
+constexpr int kHotDigits = 32;  // <= this many distinct digits in a tile: warp-aggregated atomics
 
 // Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back,
 // all kLookbackWindow loads in flight per round trip.
@@ -572,7 +601,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 st_relaxed_gpu(&lb[d], kFlagInc | tot);
             } else {
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagAgg | tot);
+#ifndef ISORT_AB_NO_LOOKBACK
                 excl = lookback_digit(lb, static_cast<int>(tile) - 1, d, 0u);
+#endif
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagInc | (excl + tot));
             }
             ISORT_TICK(q2);
