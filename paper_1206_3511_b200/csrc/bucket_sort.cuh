@@ -239,15 +239,20 @@ struct BucketState {
 // ------------------------------------------------------------------ K5
 // In-smem sort: up to 10-bit digits, two 16-bit counters per 32-bit word (a
 // stage holds < 2^16 keys, so a half never carries into the other).
-constexpr int kSegDigitBits = 10;
-constexpr int kSegWords = 1 << (kSegDigitBits - 1);
+// BLOCK threads own one counter word each in the scan: BLOCK words = 2*BLOCK bins.
+template <int BLOCK>
+struct SegDigits {
+    static constexpr int kWords = BLOCK;
+    static constexpr int kBits = BLOCK >= 1024 ? 11 : (BLOCK >= 512 ? 10 : (BLOCK >= 256 ? 9 : 8));
+    static_assert((1 << (kBits - 1)) == kWords, "power-of-two block");
+};
 
 template <typename K, int BLOCK, int IPT, bool VALS>
 struct SegSmem {
     static constexpr int kCap = BLOCK * IPT + 4;  // a stage + slack that keeps bulk copies 16-byte aligned
     alignas(16) K buf[2][kCap];                   // incoming stage / in-smem sort ping-pong
     alignas(16) uint32_t vbuf[2][VALS ? kCap : 1];
-    alignas(16) uint32_t cnt[BLOCK / 32][kSegWords];  // per-warp packed digit counters, then slot bases
+    alignas(16) uint32_t cnt[BLOCK / 32][SegDigits<BLOCK>::kWords];  // per-warp packed digit counters, then slot bases
     uint32_t scan_tot[BLOCK / 32];
     unsigned long long red[2][BLOCK / 32];
     unsigned long long pos[2];  // segment bounds, then the end of an oversized super-bucket
@@ -426,7 +431,7 @@ __device__ __forceinline__ void block_minmax2(K& lo, K& hi, unsigned long long (
 }
 
 // Stable LSD sort of ka[0, len) (payload va) in shared memory by key - kmin,
-// `passes` r-bit digits (r <= kSegDigitBits); ka/kb (va/vb) swap each pass.
+// `passes` r-bit digits (r <= SegDigits<BLOCK>::kBits); ka/kb (va/vb) swap each pass.
 // Rank primitive of the one-sweep pass: per-warp counters pre-scanned into slot
 // bases, slot = atomicAdd (lane-ordered, program-ordered => stable).  Warp w
 // owns positions [w*32*IPT, (w+1)*32*IPT); keys stay in registers between the
@@ -435,7 +440,7 @@ template <typename K, int BLOCK, int IPT, bool VALS>
 __device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K*& ka, K*& kb, uint32_t*& va,
                                         uint32_t*& vb, int len, K kmin, int passes, int r) {
     constexpr int kWarps = BLOCK / 32;
-    static_assert(kSegWords <= BLOCK, "one counter word per thread in the scan");
+    constexpr int kSegWords = SegDigits<BLOCK>::kWords;
     static_assert(BLOCK * IPT < 65536, "16-bit counters");
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
@@ -617,6 +622,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 
         // ---- stable in-smem LSD sort of ka[0, ls) by (key - min), ping-pong with the other buffer
         const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
+        constexpr int kSegDigitBits = SegDigits<BLOCK>::kBits;
         const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
         K* kb = sm.buf[cur ^ 1];
         uint32_t* vb = VALS ? sm.vbuf[cur ^ 1] : nullptr;

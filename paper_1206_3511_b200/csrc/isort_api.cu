@@ -457,8 +457,14 @@ __global__ void k_is_sorted_u32(const uint32_t* __restrict__ keys, uint64_t n, u
 
 
 // ------------------------------------------------------------- bucket sort
-constexpr int kSegBlock = 512;
-constexpr int kSegIpt = 16;
+#ifndef ISORT_SEG_BLOCK
+#define ISORT_SEG_BLOCK 512
+#endif
+#ifndef ISORT_SEG_IPT
+#define ISORT_SEG_IPT 16
+#endif
+constexpr int kSegBlock = ISORT_SEG_BLOCK;
+constexpr int kSegIpt = ISORT_SEG_IPT;
 
 struct BucketLayout {
     RadixLayout r;
@@ -484,7 +490,7 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
     auto* kern = k_bucket_segments<K, Dz, kSegBlock, kSegIpt, VALS>;
     set_max_smem_once(kern, sizeof(Smem));
     const int per_sm = resident_per_sm(kern, kSegBlock, sizeof(Smem));
-    const uint64_t want = (n + 4095) / 4096;
+    const uint64_t want = (n + kSegBlock * kSegIpt / 2 - 1) / (kSegBlock * kSegIpt / 2);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
     kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);
 }
