@@ -37,6 +37,7 @@ extern "C" {
 #define ISORT_ENOMEM 12
 #define ISORT_EINVAL 22  /* reference: std::invalid_argument */
 #define ISORT_ERANGE 34  /* n beyond the engine's per-call limit (2^30 - 1 keys) */
+#define ISORT_EIO 5      /* reference: intsort::SequenceIoError (sequence files) */
 #define ISORT_ECUDA 1001
 #define ISORT_ENCCL 1002
 
@@ -156,6 +157,30 @@ int isort_bucket_index_u64(const uint64_t* keys, uint64_t* out, uint64_t m, uint
 
 /* Device-side is_sorted (verify.hpp:12-13) over u32 keys: *result = 1/0. */
 int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* stream);
+
+/* ---- ISRT sequence files ----------------------------------
+ * Format (sequence_io.hpp:12-16): "ISRT", version 0x01, u64 LE case_id, n,
+ * range_bound, seed, then n u64 LE keys.  Errors are ISORT_EIO with the
+ * messages intsort::read_sequence throws (sequence_io.cpp:72-119). */
+typedef struct isort_sequence_header {
+    uint64_t case_id;
+    uint64_t n;
+    uint64_t range_bound;
+    uint64_t seed;
+} isort_sequence_header;
+
+/* Parse and validate the header (magic, version, truncation).  Host only. */
+int isort_sequence_read_header(const char* path, isort_sequence_header* out);
+
+/* Stream the keys of `path` into device memory `d_keys` (capacity keys of
+ * key_bytes = 4 or 8): chunks are read into pinned staging buffers, copied
+ * asynchronously and checked on the device (key > range_bound), replacing the
+ * reference's read-and-check loop (sequence_io.cpp:93-119).  The first bad key
+ * and truncation are reported exactly as the reference's 65,536-key chunked
+ * reader reports them.  key_bytes = 4 also requires every key < 2^32 (ISORT_ERANGE
+ * otherwise).  Synchronous; `*out` receives the header. */
+int isort_sequence_load(const char* path, void* d_keys, uint64_t capacity, int key_bytes,
+                        isort_sequence_header* out, int device);
 
 #ifdef __cplusplus
 }

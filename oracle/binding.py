@@ -80,6 +80,20 @@ class Oracle:
     def default_range_bound(self, case_id: int) -> int:
         return int(self.lib.orc_default_range_bound(case_id))
 
+    def write_sequence_file(self, path: str, header: tuple, records: np.ndarray) -> None:
+        """The reference's write_sequence_file (sequence_io.cpp:63-70); header = (case_id, n, M, seed)."""
+        h = (ctypes.c_uint64 * 4)(*header)
+        rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
+        self._chk(self.lib.ref_write_sequence_file(os.fsencode(path), h, rec.ctypes.data, rec.size))
+
+    def read_sequence_file(self, path: str, capacity: int = 1 << 20):
+        """The reference's read_sequence_file: ((case_id, n, M, seed), records) or
+        OracleError with the reference's SequenceIoError message."""
+        h = (ctypes.c_uint64 * 4)()
+        out = np.empty(capacity, dtype=RECORD_DTYPE)
+        self._chk(self.lib.ref_read_sequence_file(os.fsencode(path), h, out.ctypes.data, capacity))
+        return tuple(int(x) for x in h), out[: h[1]].copy()
+
     def generate(self, case_id: int, n: int, range_bound: int | None = None, seed: int = 0,
                  repeated_value: int | None = None, sorted_fraction: float = 0.95) -> np.ndarray:
         out = np.empty(n, dtype=RECORD_DTYPE)
@@ -181,6 +195,8 @@ class Reference:
             "ref_oracle_sort": (_i32, [_vp, _vp, _u64]),
             "ref_generate": (_i32, [_i32, _u64, _i32, _u64, _u64, _i32, _u64, _dbl, _vp]),
             "ref_splitmix_next": (_u64, [_u64, _u64]),
+            "ref_write_sequence_file": (_i32, [ctypes.c_char_p, ctypes.POINTER(_u64), _vp, _u64]),
+            "ref_read_sequence_file": (_i32, [ctypes.c_char_p, ctypes.POINTER(_u64), _vp, _u64]),
             "ref_time_one": (_dbl, [_i32, _vp, _u64, _u64, _u64]),
             "ref_time_sort": (_i32, [_i32, _vp, _u64, _u64, _u64, _i32, ctypes.POINTER(_dbl),
                                      ctypes.POINTER(_dbl)]),
@@ -192,6 +208,20 @@ class Reference:
     def _chk(self, rc: int) -> None:
         if rc:
             raise OracleError(self.lib.ref_last_error().decode())
+
+    def write_sequence_file(self, path: str, header: tuple, records: np.ndarray) -> None:
+        """The reference's write_sequence_file (sequence_io.cpp:63-70); header = (case_id, n, M, seed)."""
+        h = (ctypes.c_uint64 * 4)(*header)
+        rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
+        self._chk(self.lib.ref_write_sequence_file(os.fsencode(path), h, rec.ctypes.data, rec.size))
+
+    def read_sequence_file(self, path: str, capacity: int = 1 << 20):
+        """The reference's read_sequence_file: ((case_id, n, M, seed), records) or
+        OracleError with the reference's SequenceIoError message."""
+        h = (ctypes.c_uint64 * 4)()
+        out = np.empty(capacity, dtype=RECORD_DTYPE)
+        self._chk(self.lib.ref_read_sequence_file(os.fsencode(path), h, out.ctypes.data, capacity))
+        return tuple(int(x) for x in h), out[: h[1]].copy()
 
     def generate(self, case_id: int, n: int, range_bound: int | None = None, seed: int = 0,
                  repeated_value: int | None = None, sorted_fraction: float = 0.95) -> np.ndarray:

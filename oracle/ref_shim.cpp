@@ -19,6 +19,7 @@
 #include "intsort/bench.hpp"
 #include "intsort/generator.hpp"
 #include "intsort/rng.hpp"
+#include "intsort/sequence_io.hpp"
 #include "intsort/sort.hpp"
 #include "intsort/verify.hpp"
 
@@ -50,6 +51,9 @@ int guarded(F&& f) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return 22;
+    } catch (const intsort::SequenceIoError& e) {
+        g_err = e.what();
+        return 5;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 1;
@@ -114,6 +118,27 @@ int ref_generate(int case_id, std::uint64_t n, int has_range, std::uint64_t rang
         if (has_rep) spec.repeated_value = rep;
         spec.sorted_fraction = sorted_fraction;
         from_seq(intsort::generate(spec), out);
+    });
+}
+
+// write_sequence_file / read_sequence_file (sequence_io.cpp:45-128).  hdr: case_id,
+// n, range_bound, seed.  read: header always filled when it parses; records
+// only when the whole file reads (capacity permitting).
+int ref_write_sequence_file(const char* path, const std::uint64_t* hdr, const CRecord* in, std::uint64_t n) {
+    return guarded([&] {
+        intsort::write_sequence_file({hdr[0], hdr[1], hdr[2], hdr[3]}, to_seq(in, n), path);
+    });
+}
+
+int ref_read_sequence_file(const char* path, std::uint64_t* hdr, CRecord* out, std::uint64_t capacity) {
+    return guarded([&] {
+        const intsort::SequenceFile f = intsort::read_sequence_file(path);
+        hdr[0] = f.header.case_id;
+        hdr[1] = f.header.n;
+        hdr[2] = f.header.range_bound;
+        hdr[3] = f.header.seed;
+        if (f.records.size() > capacity) throw std::runtime_error("capacity");
+        from_seq(f.records, out);
     });
 }
 

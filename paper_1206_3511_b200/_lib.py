@@ -18,6 +18,7 @@ ISORT_OK = 0
 ISORT_ENOMEM = 12
 ISORT_EINVAL = 22
 ISORT_ERANGE = 34
+ISORT_EIO = 5
 ISORT_ECUDA = 1001
 ISORT_ENCCL = 1002
 
@@ -28,6 +29,13 @@ VALS_IOTA = 2
 # name -> (restype, argtypes); mirrors include/isort.h one to one.
 _u64, _u32, _i32, _sz = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
 _vp = ctypes.c_void_p
+
+
+class SequenceHeaderC(ctypes.Structure):
+    """isort_sequence_header (include/isort.h): the ISRT header fields."""
+    _fields_ = [("case_id", _u64), ("n", _u64), ("range_bound", _u64), ("seed", _u64)]
+
+
 SIGNATURES = {
     "isort_last_error": (ctypes.c_char_p, []),
     "isort_abi_version": (_i32, []),
@@ -54,6 +62,8 @@ SIGNATURES = {
     "isort_bucket_sort_host_u32": (_i32, [_vp, _vp, _u64, _u64, _i32]),
     "isort_is_sorted_u32": (_i32, [_vp, _u64, ctypes.POINTER(_i32), _vp]),
     "isort_bucket_index_u64": (_i32, [_vp, _vp, _u64, _u64, _u64, _vp]),
+    "isort_sequence_read_header": (_i32, [ctypes.c_char_p, ctypes.POINTER(SequenceHeaderC)]),
+    "isort_sequence_load": (_i32, [ctypes.c_char_p, _vp, _u64, _i32, ctypes.POINTER(SequenceHeaderC), _i32]),
 }
 
 
@@ -67,6 +77,10 @@ class IsortError(RuntimeError):
 
 class InvalidArgument(IsortError, ValueError):
     """ISORT_EINVAL: the reference throws std::invalid_argument here."""
+
+
+class SequenceIoError(IsortError):
+    """ISORT_EIO: the reference throws intsort::SequenceIoError here (sequence_io.hpp:31-33)."""
 
 
 class CudaError(IsortError):
@@ -105,6 +119,8 @@ def check(code: int) -> None:
         raise InvalidArgument(code, msg)
     if code == ISORT_ECUDA:
         raise CudaError(code, msg)
+    if code == ISORT_EIO:
+        raise SequenceIoError(code, msg)
     raise IsortError(code, msg)
 
 

@@ -105,6 +105,19 @@ def main() -> None:
         json.dump(checks, f, indent=1)
     print(f"wrote {len(meta)} small cases, {len(bidx)} bucket_index samples, {len(checks)} checksums")
 
+    # an ISRT sequence file written by the reference's own writer (sequence_io.cpp:63-70),
+    # the file of its test_sequence_io.cpp:102-113 round trip (case 6, n = 500, seed 99),
+    # plus a 2^40-range case-1 file: pins our reader and writer byte for byte
+    seqs = {}
+    for name, (case_id, n, bound, seed) in {"reference_case6.isrt": (6, 500, 1_000_000, 99),
+                                            "reference_case1_2p40.isrt": (1, 3000, 1 << 40, 7)}.items():
+        rec = ref.generate(case_id, n, bound if case_id == 1 else None, seed)
+        ref.write_sequence_file(os.path.join(HERE, name), (case_id, 0, bound, seed), rec)
+        seqs[name] = dict(case_id=case_id, n=n, range_bound=bound, seed=seed,
+                          keys_sha256=hashlib.sha256(rec["key"].astype("<u8").tobytes()).hexdigest())
+    with open(os.path.join(HERE, "reference_sequences.json"), "w") as f:
+        json.dump(seqs, f, indent=1)
+
 
 if __name__ == "__main__":
     main()
