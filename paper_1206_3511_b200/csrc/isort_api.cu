@@ -16,7 +16,10 @@
 #include <set>
 #include <utility>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <unistd.h>
 
 #include "../../include/isort.h"
 #include "bucket_sort.cuh"
@@ -723,6 +726,32 @@ int seq_staging(int device, SeqStaging** out) {
     return ISORT_OK;
 }
 
+// Read `bytes` at `offset` with several threads (page-cache reads are bound by
+// one core's copy rate, well below PCIe).
+bool pread_parallel(int fd, void* dst, uint64_t bytes, uint64_t offset) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const uint64_t parts = bytes < (8ull << 20) ? 1 : (hw >= 8 ? 8 : (hw ? hw : 1));
+    std::atomic<bool> ok{true};
+    auto work = [&](uint64_t i) {
+        const uint64_t lo = bytes * i / parts, hi = bytes * (i + 1) / parts;
+        char* p = static_cast<char*>(dst) + lo;
+        uint64_t done = 0;
+        while (done < hi - lo) {
+            const ssize_t r = pread(fd, p + done, hi - lo - done, static_cast<off_t>(offset + lo + done));
+            if (r <= 0) {
+                ok = false;
+                return;
+            }
+            done += static_cast<uint64_t>(r);
+        }
+    };
+    std::vector<std::thread> th;
+    for (uint64_t i = 1; i < parts; ++i) th.emplace_back(work, i);
+    work(0);
+    for (auto& t : th) t.join();
+    return ok;
+}
+
 template <typename K>
 int seq_load(SeqFile& sf, const char* path, const isort_sequence_header& h, K* d_keys, int device) {
     // keys the reference checks before it meets a short chunk
@@ -744,7 +773,8 @@ int seq_load(SeqFile& sf, const char* path, const isort_sequence_header& h, K* d
         const int b = static_cast<int>(c & 1);
         const uint64_t cnt = checked - off < kSeqStageKeys ? checked - off : kSeqStageKeys;
         if (c >= 2) ISORT_CUDA_TRY(cudaEventSynchronize(sg->copied[b]));  // staging buffer b is free again
-        if (fread(sg->host[b], 8, cnt, sf.f) != cnt) return seq_error("sequence file truncated in payload");
+        if (!pread_parallel(fileno(sf.f), sg->host[b], cnt * 8, kSeqHeaderBytes + off * 8))
+            return seq_error("sequence file truncated in payload");
         ISORT_CUDA_TRY(cudaMemcpyAsync(sg->dev[b], sg->host[b], cnt * 8, cudaMemcpyHostToDevice, s));
         ISORT_CUDA_TRY(cudaEventRecord(sg->copied[b], s));
         k_seq_keys<K><<<grid_for(cnt), 256, 0, s>>>(sg->dev[b], d_keys + off, cnt, off, h.range_bound, sg->flags,
