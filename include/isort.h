@@ -158,6 +158,30 @@ int isort_bucket_index_u64(const uint64_t* keys, uint64_t* out, uint64_t m, uint
 /* Device-side is_sorted (verify.hpp:12-13) over u32 keys: *result = 1/0. */
 int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* stream);
 
+/* ---- fused partition + exchange (multi-GPU, SURVEY 8e "fused variant") -------
+ * Step 1: per-destination counts of the key-range partition of keys_in (the
+ * destination-digit histogram); leaves its state in temp for step 2.
+ * counts: device u64[parts]; splitters: host, parts-1 ascending.  temp:
+ * isort_partition_temp_bytes(n, 4, ISORT_VALS_LOAD). */
+int isort_partition_counts_u32(const uint32_t* keys_in, uint64_t n, const uint32_t* splitters, int parts,
+                               uint64_t* counts, void* temp, size_t temp_bytes, void* stream);
+/* Step 2: the stable partition pass, storing destination p's keys (payload)
+ * contiguously from key_dst[p] (val_dst[p]) instead of a local send buffer --
+ * typically a slot in rank p's receive buffer opened with isort_ipc_open, so the
+ * partition writes straight over NVLink.  Same keys, splitters and temp as step
+ * 1; key_dst / val_dst are host arrays of `parts` device pointers.  The kernel
+ * ends with a system-scope fence; order the consumer after it (e.g. an NCCL
+ * all-reduce on the same stream). */
+int isort_partition_scatter_u32(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n,
+                                const uint32_t* splitters, int parts, int vals_mode, void* const* key_dst,
+                                void* const* val_dst, void* temp, size_t temp_bytes, void* stream);
+/* CUDA IPC for receive buffers: allocate + export a 64-byte handle, open a
+ * peer's handle (peer access enabled lazily), close, free. */
+int isort_ipc_alloc(size_t bytes, int device, void** ptr, unsigned char* handle);
+int isort_ipc_open(const unsigned char* handle, int device, void** ptr);
+int isort_ipc_close(void* ptr);
+int isort_ipc_free(void* ptr);
+
 /* ---- ISRT sequence files ----------------------------------
  * Format (sequence_io.hpp:12-16): "ISRT", version 0x01, u64 LE case_id, n,
  * range_bound, seed, then n u64 LE keys.  Errors are ISORT_EIO with the

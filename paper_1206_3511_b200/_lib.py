@@ -62,6 +62,12 @@ SIGNATURES = {
     "isort_bucket_sort_host_u32": (_i32, [_vp, _vp, _u64, _u64, _i32]),
     "isort_is_sorted_u32": (_i32, [_vp, _u64, ctypes.POINTER(_i32), _vp]),
     "isort_bucket_index_u64": (_i32, [_vp, _vp, _u64, _u64, _u64, _vp]),
+    "isort_partition_counts_u32": (_i32, [_vp, _u64, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "isort_partition_scatter_u32": (_i32, [_vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "isort_ipc_alloc": (_i32, [_sz, _i32, ctypes.POINTER(_vp), _vp]),
+    "isort_ipc_open": (_i32, [_vp, _i32, ctypes.POINTER(_vp)]),
+    "isort_ipc_close": (_i32, [_vp]),
+    "isort_ipc_free": (_i32, [_vp]),
     "isort_sequence_read_header": (_i32, [ctypes.c_char_p, ctypes.POINTER(SequenceHeaderC)]),
     "isort_sequence_load": (_i32, [ctypes.c_char_p, _vp, _u64, _i32, ctypes.POINTER(SequenceHeaderC), _i32]),
 }

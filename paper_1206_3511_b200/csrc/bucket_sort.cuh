@@ -663,6 +663,7 @@ namespace isort {
 // One stable pass of the one-sweep pipeline with this digitizer partitions a
 // shard by destination while keeping input order inside each destination.
 constexpr int kMaxParts = 64;
+static_assert(kMaxParts <= kScatterMax, "one scatter base per destination");
 
 template <typename K>
 struct DestDigitizer {

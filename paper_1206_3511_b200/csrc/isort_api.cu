@@ -149,7 +149,7 @@ bool rank_fast_path_ok() {
 constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
 struct RadixLayout {
-    size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
+    size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, scatter = 0, total = 0;
     uint32_t tiles = 0;
 };
 
@@ -173,6 +173,8 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
     off += align_up(n * sizeof(K));
     L.vals_alt = off;
     if (vals) off += align_up(n * sizeof(uint32_t));
+    L.scatter = off;  // per-destination bases of a scatter pass
+    off += align_up(sizeof(ScatterTable));
     L.total = off;
     return L;
 }
@@ -211,33 +213,31 @@ int resident_per_sm(F* kernel, int block, size_t smem) {
     return per_sm;
 }
 
-template <typename K, bool VALS, typename Dz, typename Cfg>
+template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false>
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
-                   uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s) {
+                   uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
+                   const ScatterTable* scat = nullptr) {
     constexpr int D = Dz::kDigits;
     using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
-    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false>
-                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true>;
+    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER>
+                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER>;
     set_max_smem_once(kern, sizeof(Smem));
     const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * kNumSMs) ? tiles
                                                                                      : Cfg::kCtasPerSm * kNumSMs;
     for (int slot = 0; slot < D; ++slot) {
         kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
-                                                        tiles, slot, dz);
+                                                        tiles, slot, dz, scat);
         static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
                                                      "pass4", "pass5", "pass6", "pass7"};
         prof_mark(s, kPassNames[slot]);
     }
 }
 
-// Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
-// bucket sort's bucket-index digits).  Buffers: kin (const) -> kout, with kalt
-// as ping-pong; the plan decides which passes run.
-template <typename K, bool VALS, typename Dz>
-int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
-                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, uint32_t* lookback,
-                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
-                          cudaStream_t s) {
+// Histogram step of a pipeline: zero the state, K1 (all digit histograms, max,
+// sortedness, range check), K2 (scans + pass plan).
+template <typename K, typename Dz>
+int launch_histogram(const K* kin, uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz,
+                     int plan_flags, bool zero_state, cudaStream_t s) {
     constexpr int D = Dz::kDigits;
     prof_mark(s, "start");
     g_prof.st = st;
@@ -256,9 +256,24 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     const unsigned grid1 = static_cast<unsigned>(want < cap1 ? (want ? want : 1) : cap1);
     k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
     prof_mark(s, "upfront");
-    k_plan<D><<<1, kRadix, 0, s>>>(st, n, skip_sorted ? 1 : 0);
+    k_plan<D><<<1, kRadix, 0, s>>>(st, n, plan_flags);
     prof_mark(s, "plan");
     launched(2);
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
+// Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
+// bucket sort's bucket-index digits).  Buffers: kin (const) -> kout, with kalt
+// as ping-pong; the plan decides which passes run.
+template <typename K, bool VALS, typename Dz>
+int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
+                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, uint32_t* lookback,
+                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
+                          cudaStream_t s) {
+    constexpr int D = Dz::kDigits;
+    int rc = launch_histogram<K, Dz>(kin, n, st, lookback, tiles, dz, skip_sorted ? kPlanSkipSorted : 0, zero_state, s);
+    if (rc) return rc;
 
     if (n < kSmallN)
         launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
@@ -636,6 +651,104 @@ int partition_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     if (rc) return rc;
     k_copy_part_counts<<<1, kMaxParts, 0, s>>>(st, counts, parts);
     launched();
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
+// Fused partition + exchange (multi-GPU step 3 + 5 in one kernel): counts first,
+// then one stable pass that stores each destination's run at its own base.
+template <typename K>
+int make_dest_digitizer(const K* splitters, int parts, DestDigitizer<K>* dz) {
+    if (parts < 1 || parts > kMaxParts)
+        return set_error(ISORT_EINVAL, "isort_partition: parts=%d outside [1, %d]", parts, kMaxParts);
+    *dz = DestDigitizer<K>{};
+    dz->nsplit = parts - 1;
+    for (int i = 0; i + 1 < parts; ++i) {
+        if (!splitters) return set_error(ISORT_EINVAL, "isort_partition: null splitters");
+        dz->split[i] = splitters[i];
+        if (i && splitters[i] < splitters[i - 1])
+            return set_error(ISORT_EINVAL, "isort_partition: splitters not ascending");
+    }
+    return ISORT_OK;
+}
+
+template <typename K>
+int partition_counts_device(const K* kin, uint64_t n, const K* splitters, int parts, uint64_t* counts, void* temp,
+                            size_t temp_bytes, cudaStream_t s) {
+    DestDigitizer<K> dz;
+    int rc = make_dest_digitizer(splitters, parts, &dz);
+    if (rc) return rc;
+    if (!counts) return set_error(ISORT_EINVAL, "isort_partition: null counts");
+    if (n == 0) {
+        ISORT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * parts, s));
+        return ISORT_OK;
+    }
+    if (n > kMaxLookbackN)
+        return set_error(ISORT_ERANGE, "isort_partition: n=%llu exceeds the per-call limit", (unsigned long long)n);
+    if (!kin) return set_error(ISORT_EINVAL, "isort_partition: null buffer");
+    const RadixLayout L = radix_layout<K>(n, true);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.state);
+    rc = launch_histogram<K>(kin, n, st, reinterpret_cast<uint32_t*>(t + L.lookback), L.tiles, dz, kPlanKeepTrivial,
+                             true, s);
+    if (rc) return rc;
+    k_copy_part_counts<<<1, kMaxParts, 0, s>>>(st, counts, parts);
+    launched();
+    ISORT_CUDA_TRY(cudaGetLastError());
+    return ISORT_OK;
+}
+
+template <typename K>
+int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, const K* splitters, int parts, int vmode,
+                             void* const* key_dst, void* const* val_dst, void* temp, size_t temp_bytes,
+                             cudaStream_t s) {
+    DestDigitizer<K> dz;
+    int rc = make_dest_digitizer(splitters, parts, &dz);
+    if (rc) return rc;
+    if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
+        return set_error(ISORT_EINVAL, "isort_partition: bad vals_mode %d", vmode);
+    if (n == 0) return ISORT_OK;
+    const bool vals = vmode != ISORT_VALS_NONE;
+    if (!kin || !key_dst || (vals && !val_dst) || (vmode == ISORT_VALS_LOAD && !vin))
+        return set_error(ISORT_EINVAL, "isort_partition: null buffer");
+    const RadixLayout L = radix_layout<K>(n, true);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    ScatterTable tbl{};
+    for (int p = 0; p < parts; ++p) {
+        tbl.key[p] = reinterpret_cast<unsigned long long>(key_dst[p]);
+        tbl.val[p] = vals ? reinterpret_cast<unsigned long long>(val_dst[p]) : 0ull;
+    }
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.state);
+    auto* scat = reinterpret_cast<ScatterTable*>(t + L.scatter);
+    ISORT_CUDA_TRY(cudaMemcpyAsync(scat, &tbl, sizeof tbl, cudaMemcpyHostToDevice, s));
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));  // `tbl` is on this stack frame
+    // the look-back words and the ticket of the (single) pass slot start from zero
+    ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * sizeof(uint32_t), s));
+    ISORT_CUDA_TRY(cudaMemsetAsync(&st->tile_ticket[0], 0, sizeof(st->tile_ticket), s));
+    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    const bool iota = vmode == ISORT_VALS_IOTA;
+    if (n < kSmallN) {
+        if (vals)
+            launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, 1>, true>(kin, nullptr, nullptr, vin, nullptr,
+                                                                              nullptr, iota, n, st, lb, L.tiles, dz, s,
+                                                                              scat);
+        else
+            launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, 1>, true>(
+                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
+    } else {
+        if (vals)
+            launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, 4>, true>(kin, nullptr, nullptr, vin, nullptr,
+                                                                              nullptr, iota, n, st, lb, L.tiles, dz, s,
+                                                                              scat);
+        else
+            launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, 4>, true>(
+                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
+    }
+    launched(1);
     ISORT_CUDA_TRY(cudaGetLastError());
     return ISORT_OK;
 }
@@ -1090,5 +1203,49 @@ int isort_sequence_load(const char* path, void* d_keys, uint64_t capacity, int k
                           : seq_load<uint64_t>(sf, path, h, static_cast<uint64_t*>(d_keys), device);
 }
 
+int isort_partition_counts_u32(const uint32_t* keys_in, uint64_t n, const uint32_t* splitters, int parts,
+                               uint64_t* counts, void* temp, size_t temp_bytes, void* stream) {
+    return partition_counts_device<uint32_t>(keys_in, n, splitters, parts, counts, temp, temp_bytes,
+                                             static_cast<cudaStream_t>(stream));
+}
+
+int isort_partition_scatter_u32(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n,
+                                const uint32_t* splitters, int parts, int vals_mode, void* const* key_dst,
+                                void* const* val_dst, void* temp, size_t temp_bytes, void* stream) {
+    return partition_scatter_device<uint32_t>(keys_in, vals_in, n, splitters, parts, vals_mode, key_dst, val_dst,
+                                              temp, temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_ipc_alloc(size_t bytes, int device, void** ptr, unsigned char* handle) {
+    if (!ptr || !handle) return set_error(ISORT_EINVAL, "isort_ipc_alloc: null argument");
+    ISORT_CUDA_TRY(cudaSetDevice(device));
+    ISORT_CUDA_TRY(cudaMalloc(ptr, bytes ? bytes : 16));
+    cudaIpcMemHandle_t h;
+    ISORT_CUDA_TRY(cudaIpcGetMemHandle(&h, *ptr));
+    static_assert(sizeof(h) == 64, "64-byte IPC handle");
+    memcpy(handle, &h, sizeof h);
+    return ISORT_OK;
+}
+
+int isort_ipc_open(const unsigned char* handle, int device, void** ptr) {
+    if (!ptr || !handle) return set_error(ISORT_EINVAL, "isort_ipc_open: null argument");
+    ISORT_CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    ISORT_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return ISORT_OK;
+}
+
+int isort_ipc_close(void* ptr) {
+    ISORT_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return ISORT_OK;
+}
+
+int isort_ipc_free(void* ptr) {
+    ISORT_CUDA_TRY(cudaFree(ptr));
+    return ISORT_OK;
+}
+
 }  // extern "C"
+
 

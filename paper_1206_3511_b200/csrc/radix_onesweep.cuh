@@ -208,10 +208,12 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
 }
 
 // ------------------------------------------------------------------- K2
-// One CTA of kRadix threads.  `allow_skip_sorted`: a sorted input needs no pass.
+// One CTA of kRadix threads.  flags: kPlanSkipSorted (a sorted input needs no
+// pass), kPlanKeepTrivial (run every digit pass, even one-digit ones: a scatter
+// pass must move the keys).
+constexpr int kPlanSkipSorted = 1, kPlanKeepTrivial = 2;
 template <int D>
-__global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, uint64_t n,
-                                                 int allow_skip_sorted) {
+__global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, uint64_t n, int flags) {
     __shared__ uint32_t warp_tot[kRadix / 32];
     __shared__ int trivial[kMaxDigits];
     const int t = threadIdx.x;
@@ -227,10 +229,11 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
         __syncthreads();
     }
     if (t == 0) {
-        const bool sorted = allow_skip_sorted && st->descents == 0;
+        const bool sorted = (flags & kPlanSkipSorted) && st->descents == 0;
+        const bool keep = (flags & kPlanKeepTrivial) != 0;
         int na = 0;
         for (int p = 0; p < D; ++p)
-            if (!sorted && !trivial[p]) st->digit_of_slot[na++] = p;
+            if (keep || (!sorted && !trivial[p])) st->digit_of_slot[na++] = p;
         for (int s = 0; s < na; ++s) {
             st->src_of_slot[s] = s == 0 ? kBufIn : st->dst_of_slot[s - 1];
             st->dst_of_slot[s] = ((na - 1 - s) % 2 == 0) ? kBufOut : kBufAlt;
@@ -284,6 +287,16 @@ struct OnesweepSmem {
     uint8_t digits[STAGE_DIGITS ? kChunk : 1];  // digit per staged key (expensive digitizers)
     uint32_t tot_w[NCHUNK][kRadix / 32];
     uint32_t tile_id;
+};
+
+// Scatter pass (fused partition + exchange): a key of digit d whose position in
+// the pass output would be g is stored at key[d] + (g - offs[d]) instead, i.e.
+// each digit's run goes to its own base pointer -- for the multi-GPU sort, a
+// slot in destination rank d's receive buffer mapped over NVLink.
+constexpr int kScatterMax = 64;
+struct ScatterTable {
+    unsigned long long key[kScatterMax];
+    unsigned long long val[kScatterMax];
 };
 
 #ifndef ISORT_LB_WINDOW
@@ -404,11 +417,13 @@ __device__ __forceinline__ void count_digit_t(uint32_t* wc, uint32_t d, bool& ag
 }
 
 // Phase 2 for one chunk.  FULL: all BLOCK*IPT keys valid (no bounds checks).
-template <bool FULL, bool AGG, bool SAFE, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
+template <bool FULL, bool AGG, bool SAFE, bool SCATTER, typename K, typename Dz, int BLOCK, int IPT, bool VALS,
+          typename Smem>
 __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restrict__ csrc,
                                                const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
                                                K* __restrict__ dst, uint64_t cbase, uint32_t valid, bool gen_iota,
-                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol) {
+                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol,
+                                               const unsigned long long* kbase, const unsigned long long* vbase) {
     const int tid = threadIdx.x;
     const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
     const K* wsrc = csrc + wofs;
@@ -444,8 +459,13 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
             const K k = sm.keys[j];
             const uint32_t d = Dz::kCheapDigit ? dz.digit_sh(k, dsh) : static_cast<uint32_t>(sm.digits[j]);
             const uint32_t g = ob[d] + j;
-            stg_hint(dst + g, k, pol);
-            if (VALS) stg_hint(vdst + g, sm.vals[j], pol);
+            if (SCATTER) {
+                *(reinterpret_cast<K*>(kbase[d]) + g) = k;
+                if (VALS) *(reinterpret_cast<uint32_t*>(vbase[d]) + g) = sm.vals[j];
+            } else {
+                stg_hint(dst + g, k, pol);
+                if (VALS) stg_hint(vdst + g, sm.vals[j], pol);
+            }
         }
     }
     __syncthreads();
@@ -515,12 +535,12 @@ __device__ __forceinline__ void onesweep_count(Smem& sm, const K* __restrict__ s
     }
 }
 
-template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE>
+template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE, bool SCATTER = false>
 __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
-               uint32_t num_tiles, int slot, Dz dz) {
+               uint32_t num_tiles, int slot, Dz dz, const ScatterTable* __restrict__ scat) {
     using Smem = OnesweepSmem<K, BLOCK, IPT, NCHUNK, VALS, !Dz::kCheapDigit>;
     constexpr int kWarps = Smem::kWarps;
     constexpr int kChunk = Smem::kChunk;
@@ -549,6 +569,12 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     const int warp = tid >> 5;
     const uint32_t lane = lane_id();
     if (tid < kRadix) sm.offs[tid] = st->offs[pos][tid];
+    __shared__ unsigned long long s_kbase[SCATTER ? kScatterMax : 1], s_vbase[SCATTER ? kScatterMax : 1];
+    if (SCATTER && tid < kScatterMax) {  // per-digit base, shifted so that base + g addresses the run
+        const unsigned long long o = st->offs[pos][tid];
+        s_kbase[tid] = scat->key[tid] - o * sizeof(K);
+        if (VALS) s_vbase[tid] = scat->val[tid] - o * sizeof(uint32_t);
+    }
 
 #ifdef ISORT_PHASE_TIMING
     long long acc[4] = {0, 0, 0, 0};
@@ -648,17 +674,17 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             const uint32_t valid = tile_len - c0 < static_cast<uint32_t>(kChunk) ? tile_len - c0 : kChunk;
             const uint64_t cbase = tile_base + c0;
             if (valid == static_cast<uint32_t>(kChunk) && hot)
-                onesweep_chunk<true, true, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                onesweep_chunk<true, true, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
                                                                           valid, gen_iota, dsh, dz, warp, lane,
-                                                                          pol_stream);
+                                                                          pol_stream, s_kbase, s_vbase);
             else if (valid == static_cast<uint32_t>(kChunk))
-                onesweep_chunk<true, false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                onesweep_chunk<true, false, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
                                                                            valid, gen_iota, dsh, dz, warp, lane,
-                                                                           pol_stream);
+                                                                           pol_stream, s_kbase, s_vbase);
             else
-                onesweep_chunk<false, false, SAFE, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
+                onesweep_chunk<false, false, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
                                                                             valid, gen_iota, dsh, dz, warp, lane,
-                                                                            pol_stream);
+                                                                            pol_stream, s_kbase, s_vbase);
         }
         ISORT_TICK(q3);
 #ifdef ISORT_PHASE_TIMING
@@ -668,6 +694,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         acc[3] += 1;
 #endif
     }
+    if (SCATTER) __threadfence_system();  // peer stores visible before the host-ordered barrier
 #ifdef ISORT_PHASE_TIMING
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));

@@ -22,7 +22,17 @@ sort is stable, so keys with equal value keep their global input order, and
 the concatenation over ranks equals the single-device stable sort bit for bit.
 
 Step 3 and 6 are CUDA kernels (via :class:`CudaOps`); steps 1-2 and 4-5 are
-collectives.  The protocol itself (:class:`KeyRangeSorter`) only talks to an
+collectives.
+
+Fused exchange (:class:`PeerBuffers`, SURVEY 8e "fused variant"): every rank's
+receive buffer is mapped into every process (CUDA IPC over NVLink/NVSwitch).
+Step 3 is split into a count (the destination-digit histogram) and the
+partition pass itself; after the G x G count matrix is gathered, the partition
+kernel stores each destination's run straight into its slot in that rank's
+receive buffer (isort_partition_scatter_u32), so steps 3 and 5 are one kernel
+and the send buffer disappears.  An on-stream all-reduce orders the local sort
+after every peer's stores.  The first distributed sort checks the fused result
+against the NCCL path bit for bit; any error or mismatch falls back to NCCL.  The protocol itself (:class:`KeyRangeSorter`) only talks to an
 ops object, which lets tests drive it over gloo on CPU with a torch-CPU stand-in
 for the kernels (tests/test_partition_gloo.py); the product path always uses
 CudaOps.
@@ -89,6 +99,41 @@ class CudaOps:
                                                 n, spl, parts, vmode, counts.data_ptr(), temp.data_ptr(), tb, s))
         return out, vout, counts
 
+    def _temp(self, n: int):
+        tb = self.lib.isort_partition_temp_bytes(n, 4, _lib.VALS_LOAD)
+        if getattr(self, "_tbuf", None) is None or self._tbuf.numel() < tb:
+            self._tbuf = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
+        return self._tbuf, tb
+
+    def partition_counts(self, keys, splitters: list[int], parts: int):
+        """Fused path, step 1: per-destination counts (state kept for step 2)."""
+        import ctypes
+
+        n = keys.numel()
+        temp, tb = self._temp(n)
+        counts = torch.zeros(parts, dtype=torch.int64, device=self.device)
+        spl = (ctypes.c_uint32 * max(1, parts - 1))(*[int(x) & 0xFFFFFFFF for x in splitters])
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.isort_partition_counts_u32(keys.data_ptr(), n, spl, parts, counts.data_ptr(),
+                                                       temp.data_ptr(), tb, s))
+        return counts
+
+    def partition_scatter(self, keys, vals, splitters: list[int], parts: int, key_dst: list[int],
+                          val_dst: list[int] | None):
+        """Fused path, step 2: the partition pass storing each destination's run at key_dst[d]."""
+        import ctypes
+
+        n = keys.numel()
+        temp, tb = self._temp(n)
+        spl = (ctypes.c_uint32 * max(1, parts - 1))(*[int(x) & 0xFFFFFFFF for x in splitters])
+        kd = (ctypes.c_void_p * parts)(*key_dst)
+        vd = (ctypes.c_void_p * parts)(*(val_dst or [0] * parts))
+        vmode = _lib.VALS_LOAD if vals is not None else _lib.VALS_NONE
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.isort_partition_scatter_u32(keys.data_ptr(), vals.data_ptr() if vals is not None else None,
+                                                        n, spl, parts, vmode, kd, vd if vals is not None else None,
+                                                        temp.data_ptr(), tb, s))
+
     def local_sort(self, keys, vals, algorithm: str, lo: int, hi: int):
         from . import device
 
@@ -111,16 +156,114 @@ class CudaOps:
         return a.elapsed_time(b)
 
 
+def recv_totals(matrix: list[list[int]]) -> list[int]:
+    """Keys each rank receives: column sums of the count matrix (row = source)."""
+    g = len(matrix)
+    return [sum(matrix[src][d] for src in range(g)) for d in range(g)]
+
+
+def fused_destinations(matrix: list[list[int]], me: int, bases: list[int], elem_bytes: int) -> list[int]:
+    """Device address where rank `me`'s run for destination d starts: d's receive
+    buffer + the keys of lower source ranks (chunks land in source-rank order)."""
+    g = len(matrix)
+    return [bases[d] + elem_bytes * sum(matrix[src][d] for src in range(me)) for d in range(g)]
+
+
+class _CudaArray:
+    """A raw device pointer seen as a tensor (torch.as_tensor via __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def device_view(ptr: int, n: int, device) -> torch.Tensor:
+    if n == 0:
+        return torch.empty(0, dtype=torch.int32, device=device)
+    return torch.as_tensor(_CudaArray(ptr, n), device=device)
+
+
+class PeerBuffers:
+    """Receive buffers (keys + u32 payload) of all ranks, mapped into this process.
+
+    Each rank allocates `capacity` keys with isort_ipc_alloc, the 64-byte IPC
+    handles are all-gathered, and every peer's buffers are opened with
+    isort_ipc_open (peer access over NVLink).  `key_bases[r]` / `val_bases[r]`
+    are device addresses usable by this rank's kernels."""
+
+    def __init__(self, dist, device: torch.device, capacity: int):
+        import ctypes
+
+        self.lib = _lib.load()
+        self.dist, self.device, self.capacity = dist, device, capacity
+        g, me = dist.get_world_size(), dist.get_rank()
+        self.own, self.opened, handles = [], [], []
+        ok = torch.ones(1, dtype=torch.int32, device=device)
+        try:
+            for _ in range(2):  # keys, payload
+                ptr = ctypes.c_void_p()
+                h = (ctypes.c_ubyte * 64)()
+                _lib.check(self.lib.isort_ipc_alloc(4 * max(capacity, 1), device.index, ctypes.byref(ptr), h))
+                self.own.append(int(ptr.value))
+                handles.append(bytes(h))
+        except _lib.IsortError:
+            ok.zero_()
+            handles = [bytes(64), bytes(64)]
+        self._agree(ok, "allocate")  # every rank takes the same branch before the next collective
+        mine = torch.tensor(list(handles[0] + handles[1]), dtype=torch.uint8, device=device)
+        allh = [torch.zeros_like(mine) for _ in range(g)]
+        dist.all_gather(allh, mine)
+        self.key_bases, self.val_bases = [], []
+        try:
+            for r in range(g):
+                if r == me:
+                    self.key_bases.append(self.own[0])
+                    self.val_bases.append(self.own[1])
+                    continue
+                raw = bytes(allh[r].cpu().tolist())
+                ptrs = []
+                for i in range(2):
+                    ptr = ctypes.c_void_p()
+                    hb = (ctypes.c_ubyte * 64).from_buffer_copy(raw[64 * i: 64 * (i + 1)])
+                    _lib.check(self.lib.isort_ipc_open(hb, device.index, ctypes.byref(ptr)))
+                    self.opened.append(int(ptr.value))
+                    ptrs.append(int(ptr.value))
+                self.key_bases.append(ptrs[0])
+                self.val_bases.append(ptrs[1])
+        except _lib.IsortError:
+            ok.zero_()
+        self._agree(ok, "open")
+
+    def _agree(self, ok: torch.Tensor, what: str) -> None:
+        self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
+        if not bool(ok.item()):
+            self.close()
+            raise RuntimeError(f"PeerBuffers: some rank could not {what} its CUDA IPC buffers")
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        if self.dist.get_world_size() > 1:
+            self.dist.barrier()  # no peer still writes into our buffers
+        for p in self.opened:
+            self.lib.isort_ipc_close(p)
+        for p in self.own:
+            self.lib.isort_ipc_free(p)
+        self.opened, self.own = [], []
+
+
 class KeyRangeSorter:
     """Distributed stable sort of u32 keys (+ optional u32 payload) over a process group."""
 
-    def __init__(self, dist, ops, sample_per_rank: int = DEFAULT_SAMPLE, key_max: int = 0xFFFFFFFF):
+    def __init__(self, dist, ops, sample_per_rank: int = DEFAULT_SAMPLE, key_max: int = 0xFFFFFFFF,
+                 peers: PeerBuffers | None = None):
         self.dist = dist
         self.ops = ops
         self.world = dist.get_world_size()
         self.rank = dist.get_rank()
         self.sample_per_rank = sample_per_rank
         self.key_max = key_max
+        self.peers = peers  # fused partition + exchange when set
+        self.last_path = None
 
     def splitters(self, keys: torch.Tensor) -> list[int]:
         """G-1 ascending splitter key values from the gathered sample's quantiles."""
@@ -149,19 +292,50 @@ class KeyRangeSorter:
             out[i] = max(out[i], out[i - 1])
         return out
 
-    def sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None, algorithm: str = "radix"):
+    def _fused_exchange(self, keys, vals, spl):
+        """Counts -> gathered count matrix -> partition pass storing into the peers'
+        receive buffers -> on-stream barrier.  Returns (keys, payload) views of this
+        rank's receive buffer, or None when some rank's share exceeds the capacity."""
+        g, me, pb = self.world, self.rank, self.peers
+        counts = self.ops.partition_counts(keys, spl, g)
+        allc = [torch.zeros_like(counts) for _ in range(g)]
+        self.dist.all_gather(allc, counts)
+        matrix = [[int(x) for x in row.tolist()] for row in allc]
+        totals = recv_totals(matrix)
+        if max(totals) > pb.capacity:
+            return None
+        kd = fused_destinations(matrix, me, pb.key_bases, 4)
+        vd = fused_destinations(matrix, me, pb.val_bases, 4) if vals is not None else None
+        self.ops.partition_scatter(keys, vals, spl, g, kd, vd)
+        flag = torch.zeros(1, dtype=torch.int32, device=keys.device)
+        self.dist.all_reduce(flag)  # every peer's stores precede the local sort
+        out = device_view(pb.key_bases[me], totals[me], keys.device)
+        vout = device_view(pb.val_bases[me], totals[me], keys.device) if vals is not None else None
+        return out, vout
+
+    def sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None, algorithm: str = "radix",
+             force_nccl: bool = False):
         """Returns (this rank's sorted key range, payload or None, PhaseTimes)."""
         g, me = self.world, self.rank
         pt = PhaseTimes()
         e0 = self.ops.event()
         spl = self.splitters(keys)
         e1 = self.ops.event()
-        if g > 1:
+        fused = None
+        if g > 1 and self.peers is not None and not force_nccl:
+            fused = self._fused_exchange(keys, vals, spl)  # None: does not fit, use NCCL
+        if g > 1 and fused is None:
             parted, pvals, counts = self.ops.partition(keys, vals, spl, g)
+            self.last_path = "nccl"
+        elif g > 1:
+            parted, pvals, counts = None, None, None
+            self.last_path = "fused"
         else:
             parted, pvals, counts = keys, vals, None
         e2 = self.ops.event()
-        if g > 1:
+        if g > 1 and fused is not None:
+            out, vout = fused
+        elif g > 1:
             # count matrix: row = source rank, column = destination rank
             allc = [torch.zeros_like(counts) for _ in range(g)]
             self.dist.all_gather(allc, counts)
@@ -189,13 +363,42 @@ class KeyRangeSorter:
         return sk, sv, pt
 
 
+def enable_fused(sorter: KeyRangeSorter, keys: torch.Tensor, algorithm: str, slack: float = 1.5) -> bool:
+    """Map the receive buffers (capacity = slack x the local shard) and switch the
+    sorter to the fused exchange if one trial sort matches the NCCL path bit for
+    bit on every rank; otherwise (IPC unavailable, mismatch) keep NCCL."""
+    dist, dev = sorter.dist, keys.device
+    try:
+        sorter.peers = PeerBuffers(dist, dev, int(slack * keys.numel()) + (1 << 16))
+    except RuntimeError:  # raised on every rank alike
+        sorter.peers = None
+        return False
+    ok = torch.ones(1, dtype=torch.int32, device=dev)
+    pos = torch.arange(keys.numel(), dtype=torch.int32, device=dev)
+    a_k, a_v, _ = sorter.sort(keys, pos, algorithm=algorithm)
+    path = sorter.last_path
+    a_k, a_v = a_k.clone(), a_v.clone()
+    b_k, b_v, _ = sorter.sort(keys, pos, algorithm=algorithm, force_nccl=True)
+    if path != "fused" or not (torch.equal(a_k, b_k) and torch.equal(a_v, b_v)):
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not bool(ok.item()):
+        sorter.peers.close()
+        sorter.peers = None
+    return sorter.peers is not None
+
+
 def bench_distributed(keys: torch.Tensor, algorithm: str, range_bound: int, steps: int, warmup: int, dist):
     """Time `steps` distributed sorts of the per-rank shards (bench.py, N > 1).
 
     Device time per step = max over ranks of (CUDA-event time from the first
     barrier to the end of the local sort).  Returns (ms_per_step, info)."""
+    import os
+
     dev = keys.device
     sorter = KeyRangeSorter(dist, CudaOps(dev))
+    if os.environ.get("ISORT_FUSED_EXCHANGE", "1") != "0":
+        enable_fused(sorter, keys, algorithm)
     l0 = _lib.load().isort_launch_count()
     for _ in range(warmup):
         sorter.sort(keys, algorithm=algorithm)
@@ -223,7 +426,9 @@ def bench_distributed(keys: torch.Tensor, algorithm: str, range_bound: int, step
     dist.all_reduce(mean, op=dist.ReduceOp.SUM)
     info = {"phases": {k: round(v, 4) for k, v in avg.items()}, "launches": int(launches),
             "max_over_mean_received": float(mx.item() / max(1.0, mean.item() / dist.get_world_size())),
-            "warmup_launches": int(l1 - l0)}
+            "warmup_launches": int(l1 - l0),
+            "exchange": "fused (partition stores into peer receive buffers over NVLink)" if sorter.peers is not None
+            else "nccl all_to_all"}
     return float(ms.item()), info
 
 

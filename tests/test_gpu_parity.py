@@ -296,6 +296,48 @@ def test_partition_kernel_is_stable_grouping(cuda, parts):
         assert np.array_equal(ov.cpu().numpy(), v[order]), (parts, n)
 
 
+@pytest.mark.parametrize("parts", [2, 5, 8])
+def test_fused_partition_scatter_protocol(cuda, oracle, parts):
+    """The fused exchange's kernels and address arithmetic on one GPU: `parts`
+    simulated ranks run one after another (no kernel waits on another).  Each
+    counts its shard, the count matrix gives every run's slot, and the partition
+    pass stores each run straight into the destination's receive buffer; the
+    destinations' stable local sorts concatenate to the global stable sort."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+    from paper_1206_3511_b200.partition import CudaOps, fused_destinations, recv_totals
+
+    rng = np.random.default_rng(100 + parts)
+    n = 2_500_000 + parts * 7919
+    keys = oracle.mixture_u32(n, 40 + parts)
+    pos = np.arange(n, dtype=np.int32)
+    shards = np.array_split(np.arange(n), parts)
+    spl = sorted(int(x) for x in np.quantile(keys[rng.integers(0, n, 4096)], np.arange(1, parts) / parts))
+    ops = [CudaOps(torch.device("cuda:0")) for _ in range(parts)]
+    tk = [torch.from_numpy(keys[sh].view(np.int32)).cuda() for sh in shards]
+    tv = [torch.from_numpy(pos[sh]).cuda() for sh in shards]
+    matrix = [[int(c) for c in ops[r].partition_counts(tk[r], spl, parts).tolist()] for r in range(parts)]
+    totals = recv_totals(matrix)
+    assert sum(totals) == n
+    rk = [torch.full((t + 3,), -1, dtype=torch.int32, device="cuda") for t in totals]  # + guard words
+    rv = [torch.full((t + 3,), -1, dtype=torch.int32, device="cuda") for t in totals]
+    kb, vb = [t.data_ptr() for t in rk], [t.data_ptr() for t in rv]
+    for r in range(parts):
+        ops[r].partition_scatter(tk[r], tv[r], spl, parts, fused_destinations(matrix, r, kb, 4),
+                                 fused_destinations(matrix, r, vb, 4))
+    torch.cuda.synchronize()
+    got_k, got_v = [], []
+    for d in range(parts):
+        assert (rk[d][totals[d]:] == -1).all() and (rv[d][totals[d]:] == -1).all(), "store past the slot"
+        k, v = device.radix_sort(rk[d][: totals[d]].contiguous(), vals=rv[d][: totals[d]].contiguous())
+        got_k.append(k.cpu().numpy().view(np.uint32))
+        got_v.append(v.cpu().numpy())
+    want_k, want_i = oracle.sort_u32(keys, with_index=True)
+    assert np.array_equal(np.concatenate(got_k), want_k)
+    assert np.array_equal(np.concatenate(got_v).astype(np.uint32), want_i)
+
+
 def test_key_range_protocol_single_rank_gpu(cuda, oracle):
     """World size 1 through the same protocol object (no exchange), GPU kernels."""
     import torch

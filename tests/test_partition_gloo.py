@@ -116,3 +116,19 @@ def test_splitters_balance_uniform(tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), "uniform", str(tmp_path)), nprocs=world, join=True)
     sizes = [np.load(tmp_path / f"k{r}.npy").size for r in range(world)]
     assert max(sizes) / (sum(sizes) / world) < 1.15
+
+
+def test_fused_exchange_addresses():
+    """Slots of the fused exchange: destination d receives the runs of sources
+    0..G-1 back to back, in source order (= global input order)."""
+    from paper_1206_3511_b200.partition import fused_destinations, recv_totals
+
+    m = [[3, 0, 5], [1, 2, 0], [4, 4, 4]]  # row = source, column = destination
+    assert recv_totals(m) == [8, 6, 9]
+    bases = [1000, 2000, 3000]
+    assert fused_destinations(m, 0, bases, 4) == [1000, 2000, 3000]
+    assert fused_destinations(m, 1, bases, 4) == [1000 + 12, 2000, 3000 + 20]
+    assert fused_destinations(m, 2, bases, 4) == [1000 + 16, 2000 + 8, 3000 + 20]
+    for d in range(3):  # the last source's run ends exactly at the destination's total
+        last = fused_destinations(m, 2, bases, 4)[d] + 4 * m[2][d]
+        assert last == bases[d] + 4 * recv_totals(m)[d]
