@@ -416,19 +416,14 @@ __device__ __forceinline__ void count_digit_t(uint32_t* wc, uint32_t d, bool& ag
     atomicAdd(&wc[d], 1u);
 }
 
-// Phase 2 for one chunk.  FULL: all BLOCK*IPT keys valid (no bounds checks).
-template <bool FULL, bool AGG, bool SAFE, bool SCATTER, typename K, typename Dz, int BLOCK, int IPT, bool VALS,
-          typename Smem>
-__device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restrict__ csrc,
-                                               const uint32_t* __restrict__ vsrc, uint32_t* __restrict__ vdst,
-                                               K* __restrict__ dst, uint64_t cbase, uint32_t valid, bool gen_iota,
-                                               uint32_t dsh, const Dz& dz, int warp, uint32_t lane, uint64_t pol,
-                                               const unsigned long long* kbase, const unsigned long long* vbase) {
-    const int tid = threadIdx.x;
+// Phase 2 of one chunk, in three steps so the next chunk's loads are in flight
+// while this chunk is written out.  FULL: all BLOCK*IPT keys valid.
+template <bool FULL, typename K, int BLOCK, int IPT, bool VALS>
+__device__ __forceinline__ void chunk_load(K (&key)[IPT], uint32_t (&val)[VALS ? IPT : 1], const K* __restrict__ csrc,
+                                           const uint32_t* __restrict__ vsrc, uint64_t cbase, uint32_t valid,
+                                           bool gen_iota, int warp, uint32_t lane, uint64_t pol) {
     const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
     const K* wsrc = csrc + wofs;
-    K key[IPT];
-    uint32_t val[VALS ? IPT : 1];
 #pragma unroll
     for (int i = 0; i < IPT; ++i)
         key[i] = (FULL || wofs + i * 32u < valid) ? ldg_hint(wsrc + i * 32, pol) : static_cast<K>(0);
@@ -438,6 +433,12 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
             val[i] = gen_iota ? static_cast<uint32_t>(cbase + wofs + i * 32u)
                               : ((FULL || wofs + i * 32u < valid) ? ldg_stream(vsrc + cbase + wofs + i * 32u) : 0u);
     }
+}
+
+template <bool FULL, bool AGG, bool SAFE, typename K, typename Dz, int IPT, bool VALS, typename Smem>
+__device__ __forceinline__ void chunk_rank(Smem& sm, int c, const K (&key)[IPT], const uint32_t (&val)[VALS ? IPT : 1],
+                                           uint32_t valid, uint32_t dsh, const Dz& dz, int warp, uint32_t lane) {
+    const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
     uint32_t* wc = sm.cnt[c][warp];
     bool agg = FULL && AGG;
 #pragma unroll
@@ -450,7 +451,13 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
             if (!Dz::kCheapDigit) sm.digits[s] = static_cast<uint8_t>(d);
         }
     }
-    __syncthreads();
+}
+
+template <bool FULL, bool SCATTER, typename K, typename Dz, int BLOCK, int IPT, bool VALS, typename Smem>
+__device__ __forceinline__ void chunk_write(Smem& sm, int c, K* __restrict__ dst, uint32_t* __restrict__ vdst,
+                                            uint32_t valid, uint32_t dsh, const Dz& dz, uint64_t pol,
+                                            const unsigned long long* kbase, const unsigned long long* vbase) {
+    const int tid = threadIdx.x;
     const uint32_t* ob = sm.out_base[c];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -468,7 +475,6 @@ __device__ __forceinline__ void onesweep_chunk(Smem& sm, int c, const K* __restr
             }
         }
     }
-    __syncthreads();
 }
 
 // Phase 1: per-(chunk, warp) digit counts of one tile (keys via L2, kept there
@@ -667,24 +673,41 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         hot_prev = hot;
 
         // ---------------- phase 2: stage by slot, coalesced scatter
+        K key[IPT];
+        uint32_t val[VALS ? IPT : 1];
+        auto load = [&](int c) {
+            const uint32_t c0 = static_cast<uint32_t>(c) * kChunk;
+            const uint32_t valid = tile_len - c0 < static_cast<uint32_t>(kChunk) ? tile_len - c0 : kChunk;
+            const uint64_t cbase = tile_base + c0;
+            if (valid == static_cast<uint32_t>(kChunk))
+                chunk_load<true, K, BLOCK, IPT, VALS>(key, val, src + cbase, vsrc, cbase, valid, gen_iota, warp, lane,
+                                                      pol_stream);
+            else
+                chunk_load<false, K, BLOCK, IPT, VALS>(key, val, src + cbase, vsrc, cbase, valid, gen_iota, warp, lane,
+                                                       pol_stream);
+        };
+        load(0);
 #pragma unroll 1
         for (int c = 0; c < NCHUNK; ++c) {
             const uint32_t c0 = static_cast<uint32_t>(c) * kChunk;
             if (c0 >= tile_len) break;
             const uint32_t valid = tile_len - c0 < static_cast<uint32_t>(kChunk) ? tile_len - c0 : kChunk;
-            const uint64_t cbase = tile_base + c0;
-            if (valid == static_cast<uint32_t>(kChunk) && hot)
-                onesweep_chunk<true, true, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
-                                                                          valid, gen_iota, dsh, dz, warp, lane,
-                                                                          pol_stream, s_kbase, s_vbase);
-            else if (valid == static_cast<uint32_t>(kChunk))
-                onesweep_chunk<true, false, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
-                                                                           valid, gen_iota, dsh, dz, warp, lane,
-                                                                           pol_stream, s_kbase, s_vbase);
+            const bool full = valid == static_cast<uint32_t>(kChunk);
+            if (full && hot)
+                chunk_rank<true, true, SAFE, K, Dz, IPT, VALS>(sm, c, key, val, valid, dsh, dz, warp, lane);
+            else if (full)
+                chunk_rank<true, false, SAFE, K, Dz, IPT, VALS>(sm, c, key, val, valid, dsh, dz, warp, lane);
             else
-                onesweep_chunk<false, false, SAFE, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, src + cbase, vsrc, vdst, dst, cbase,
-                                                                            valid, gen_iota, dsh, dz, warp, lane,
-                                                                            pol_stream, s_kbase, s_vbase);
+                chunk_rank<false, false, SAFE, K, Dz, IPT, VALS>(sm, c, key, val, valid, dsh, dz, warp, lane);
+            if (c + 1 < NCHUNK && c0 + kChunk < tile_len) load(c + 1);  // in flight during the write-out
+            __syncthreads();
+            if (full)
+                chunk_write<true, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, dst, vdst, valid, dsh, dz, pol_stream,
+                                                                    s_kbase, s_vbase);
+            else
+                chunk_write<false, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, dst, vdst, valid, dsh, dz, pol_stream,
+                                                                     s_kbase, s_vbase);
+            __syncthreads();
         }
         ISORT_TICK(q3);
 #ifdef ISORT_PHASE_TIMING
