@@ -231,6 +231,9 @@ def profile_phases(lib):
 
 
 def time_device_sort(sorter, keys, steps, warmup, lib, dist=None):
+    """K timed steps (CUDA events on the sort's stream) for the value, then K more
+    with per-kernel events between launches (isort_profile_*) for the phases and
+    the roofline: the events add launch gaps, so they stay out of the value."""
     import torch
 
     for _ in range(warmup):
@@ -240,18 +243,22 @@ def time_device_sort(sorter, keys, steps, warmup, lib, dist=None):
         dist.barrier()
     torch.cuda.synchronize()
     l0 = lib.isort_launch_count()
-    lib.isort_profile_begin()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for _ in range(steps):
         sorter(keys)
     end.record()
     torch.cuda.synchronize()
-    phases, n_active = profile_phases(lib)
     launches = lib.isort_launch_count() - l0
+    ms = start.elapsed_time(end) / steps
+    lib.isort_profile_begin()
+    for _ in range(steps):
+        sorter(keys)
+    torch.cuda.synchronize()
+    phases, n_active = profile_phases(lib)
     if dist is not None:
         dist.barrier()
-    return start.elapsed_time(end) / steps, phases, n_active, launches
+    return ms, phases, n_active, launches
 
 
 def pass_stats(phases, steps, n_active):
