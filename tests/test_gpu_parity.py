@@ -338,6 +338,28 @@ def test_fused_partition_scatter_protocol(cuda, oracle, parts):
     assert np.array_equal(np.concatenate(got_v).astype(np.uint32), want_i)
 
 
+@pytest.mark.parametrize("n", [1000, 1_000_000, 5_000_003])
+def test_radix_cuda_graph_replay(cuda, oracle, n):
+    """Sorter(graph=True): eager first call, then capture, then replays that read
+    the (same) input buffer afresh -- bit-exact every time."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(n)
+    s = device.Sorter(n, 4, "radix", "iota", graph=True)
+    buf = torch.empty(n, dtype=torch.int32, device="cuda")
+    for it in range(4):
+        k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        buf.copy_(torch.from_numpy(k.view(np.int32)))
+        ko, vo = s(buf)
+        torch.cuda.synchronize()
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        assert np.array_equal(ko.cpu().numpy().view(np.uint32), want_k), it
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), want_i), it
+    assert s._graph is not None and s.launches_per_call >= 3
+
+
 def test_key_range_protocol_single_rank_gpu(cuda, oracle):
     """World size 1 through the same protocol object (no exchange), GPU kernels."""
     import torch
