@@ -86,3 +86,119 @@ def config_keys(name: str, n: int | None = None, seed: int = 42) -> np.ndarray:
 def config_range_bound(name: str) -> int:
     """Inclusive key bound the bucket sort partitions against, per config."""
     return 1023 if name.lower() == "c3" else (1 << 32) - 1
+
+
+# ------------------------------------------------- the reference's six input cases
+# generate() (generator.cpp:112-147) over SplitMix64::below (rng.hpp:25-38), exact:
+# x_k = mix(seed + (k+1)*gamma) is counter-based, and a rejected draw only skips
+# one x, so a batch of draws = the accepted values of a slightly longer batch.
+_U64MAX = (1 << 64) - 1
+
+
+class _Stream:
+    def __init__(self, seed: int):
+        self.seed, self.ctr = seed, 0
+
+    def raw(self, m: int) -> np.ndarray:
+        out = _stream(self.seed, self.ctr, m, offset=1)
+        self.ctr += m
+        return out
+
+    def below(self, bound: int, m: int) -> np.ndarray:
+        """m draws of below(bound) (the same bound)."""
+        if bound <= 0:
+            raise ValueError("SplitMix64::below: bound must be >= 1")
+        lim = np.uint64(_U64MAX - ((1 << 64) - bound) % bound)
+        got, parts = 0, []
+        while got < m:
+            want = m - got
+            xs = _stream(self.seed, self.ctr, want + 8, offset=1)
+            ok = np.flatnonzero(xs <= lim)[:want]
+            take = xs[ok]
+            self.ctr += int(ok[-1]) + 1 if ok.size else want + 8
+            parts.append(take % np.uint64(bound))
+            got += take.size
+        return np.concatenate(parts) if parts else np.empty(0, dtype=np.uint64)
+
+    def below_each(self, bounds: np.ndarray) -> np.ndarray:
+        """One draw per element, bound bounds[i] (varying), in order."""
+        out = np.empty(bounds.size, dtype=np.uint64)
+        i = 0
+        b64 = bounds.astype(np.uint64)
+        while i < bounds.size:
+            rest = b64[i:]
+            xs = _stream(self.seed, self.ctr, rest.size, offset=1)
+            with np.errstate(over="ignore"):
+                lim = np.uint64(_U64MAX) - ((np.uint64(0) - rest) % rest)
+            bad = np.flatnonzero(xs > lim)
+            r = int(bad[0]) if bad.size else rest.size
+            out[i:i + r] = xs[:r] % rest[:r]
+            self.ctr += r + (1 if bad.size else 0)  # the rejected x is skipped, its bound redrawn
+            i += r
+        return out
+
+
+def _mulmod(j: np.ndarray, s: int, m: int) -> np.ndarray:
+    """(j * s) mod m without 128-bit products: j < 2^27, s, m < 2^41."""
+    jl = j & np.uint64((1 << 20) - 1)
+    jh = j >> np.uint64(20)
+    a = np.uint64(((1 << 20) * s) % m)
+    return ((jh * a) % np.uint64(m) + (jl * np.uint64(s)) % np.uint64(m)) % np.uint64(m)
+
+
+def default_range_bound(case_id: int) -> int:  # generator.cpp:71-80
+    return {4: 10_000, 5: 100_000_000}.get(case_id, 1_000_000)
+
+
+def generate_case(case_id: int, n: int, range_bound: int | None = None, seed: int = 0,
+                  repeated_value: int | None = None, sorted_fraction: float = 0.95) -> np.ndarray:
+    """Keys (uint64) of the reference's generate(InputSpec) -- exact for all six
+    cases (tests/test_inputs.py pins it against the reference).  Cases 3 and 6
+    end in sequential swap loops and are meant for n up to ~10^7."""
+    import math
+
+    if case_id < 1 or case_id > 6:
+        raise ValueError("InputSpec: case_id must be in 1..6")
+    bound = default_range_bound(case_id) if range_bound is None else int(range_bound)
+    if bound > (1 << 40):
+        raise ValueError("InputSpec: range_bound exceeds 2^40")
+    if not 0.0 <= sorted_fraction <= 1.0:
+        raise ValueError("InputSpec: sorted_fraction must be in [0, 1]")
+    rng = _Stream(seed)
+    if case_id in (1, 4, 5):
+        return rng.below(bound + 1, n)
+    if case_id in (2, 3):
+        keys = np.sort(rng.below(bound + 1, n))
+        if case_id == 3:
+            swaps = int((1.0 - sorted_fraction) * float(n))
+            ab = rng.below(n, 2 * swaps) if swaps else np.empty(0, dtype=np.uint64)
+            k = keys.tolist()
+            for a, b in zip(ab[0::2].tolist(), ab[1::2].tolist()):
+                k[a], k[b] = k[b], k[a]
+            keys = np.array(k, dtype=np.uint64)
+        return keys
+    # case 6: ceil(n/3) copies of the repeated value + distinct fillers on a coprime walk, shuffled
+    rep = bound // 2 if repeated_value is None else int(repeated_value)
+    if rep > bound:
+        raise ValueError("InputSpec: repeated_value exceeds range_bound")
+    if (2 * n + 2) // 3 > bound:
+        raise ValueError(f"InputSpec: case 6 infeasible, ceil(2n/3) = {(2 * n + 2) // 3} exceeds range_bound {bound} "
+                         "(not enough distinct values)")
+    dup = (n + 2) // 3
+    distinct = n - dup
+    m = bound + 1
+    keys = np.full(n, rep, dtype=np.uint64)
+    if distinct > 0:
+        while True:
+            stride = int(rng.below(m, 1)[0])
+            if stride != 0 and math.gcd(stride, m) == 1:
+                break
+        v = int(rng.below(m, 1)[0])
+        walk = (np.uint64(v) + _mulmod(np.arange(distinct + 1, dtype=np.uint64), stride, m)) % np.uint64(m)
+        walk = walk[walk != np.uint64(rep)][:distinct]
+        keys[dup:] = walk
+    js = rng.below_each(np.arange(n, 1, -1, dtype=np.uint64))  # Fisher-Yates, i = n .. 2
+    k = keys.tolist()
+    for i, j in zip(range(n, 1, -1), js.tolist()):
+        k[i - 1], k[j] = k[j], k[i - 1]
+    return np.array(k, dtype=np.uint64)
