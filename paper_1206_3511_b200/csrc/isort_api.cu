@@ -87,21 +87,32 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 // kSmallN use 1-chunk tiles so a few million keys still fill all SMs.
 constexpr uint64_t kSmallN = 4ull << 20;
 
-template <typename K, bool VALS, int CHUNKS = 4>
+#ifndef ISORT_PASS_CHUNKS
+#define ISORT_PASS_CHUNKS 2
+#endif
+template <typename K, bool VALS, int CHUNKS = ISORT_PASS_CHUNKS>
 struct PassCfg {
     static constexpr int kBlock = ISORT_PASS_BLOCK;
 #ifndef ISORT_PASS_IPT32
-#define ISORT_PASS_IPT32 12
+#define ISORT_PASS_IPT32 24
 #endif
-    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? 8 : ISORT_PASS_IPT32) : (VALS ? 6 : 8);
+#ifndef ISORT_PASS_IPT32V
+#define ISORT_PASS_IPT32V 12
+#endif
+#ifndef ISORT_PASS_IPT64
+#define ISORT_PASS_IPT64 12
+#endif
+    // keys per thread per chunk; the 1-chunk small-n tile keeps 12 (more tiles)
+    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? ISORT_PASS_IPT32V : (CHUNKS == 1 ? 12 : ISORT_PASS_IPT32))
+                                               : (VALS ? 6 : ISORT_PASS_IPT64);
     static constexpr int kChunks = CHUNKS;
     static constexpr int kTile = kBlock * kIpt * kChunks;
-    static constexpr int kCtasPerSm = 1024 / kBlock;
+    static constexpr int kCtasPerSm = ISORT_PASS_MINB_OF(kBlock);
 };
 
 template <typename K, bool VALS>
 inline int pass_tile(uint64_t n) {
-    return n < kSmallN ? PassCfg<K, VALS, 1>::kTile : PassCfg<K, VALS, 4>::kTile;
+    return n < kSmallN ? PassCfg<K, VALS, 1>::kTile : PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
 }
 
 // Upfront histogram replication (lane copies per bin): 64 KB of counters.
@@ -279,7 +290,7 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
         launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
                                                         dz, s);
     else
-        launch_passes<K, VALS, Dz, PassCfg<K, VALS, 4>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
+        launch_passes<K, VALS, Dz, PassCfg<K, VALS, ISORT_PASS_CHUNKS>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
                                                         dz, s);
     launched(D);
     const uint64_t cblocks = (n + 4095) / 4096;
@@ -741,11 +752,11 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
                 kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
     } else {
         if (vals)
-            launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, 4>, true>(kin, nullptr, nullptr, vin, nullptr,
+            launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, ISORT_PASS_CHUNKS>, true>(kin, nullptr, nullptr, vin, nullptr,
                                                                               nullptr, iota, n, st, lb, L.tiles, dz, s,
                                                                               scat);
         else
-            launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, 4>, true>(
+            launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, ISORT_PASS_CHUNKS>, true>(
                 kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
     }
     launched(1);

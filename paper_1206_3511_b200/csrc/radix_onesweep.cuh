@@ -299,6 +299,13 @@ struct ScatterTable {
     unsigned long long val[kScatterMax];
 };
 
+// Resident one-sweep CTAs per SM (the launch bound's minimum and the grid size).
+#ifndef ISORT_PASS_MINB
+#define ISORT_PASS_MINB_OF(block) (1024 / (block))
+#else
+#define ISORT_PASS_MINB_OF(block) ISORT_PASS_MINB
+#endif
+
 #ifndef ISORT_LB_WINDOW
 #define ISORT_LB_WINDOW 16
 #endif
@@ -542,7 +549,7 @@ __device__ __forceinline__ void onesweep_count(Smem& sm, const K* __restrict__ s
 }
 
 template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bool SAFE, bool SCATTER = false>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+__global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,

@@ -16,10 +16,12 @@ from oracle.binding import RECORD_DTYPE
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 U32_MAX = (1 << 32) - 1
-# one-sweep geometry: chunk = 512 threads x IPT keys, tile = 4 chunks
-# (keys-only IPT 12: 6144 / 24576; with payload IPT 8: 4096 / 16384)
+# one-sweep geometry: chunk = 512 threads x IPT keys, tile = 2 chunks
+# (keys-only IPT 24: 12288 / 24576; with payload IPT 12: 6144 / 12288; below 4M keys
+# one 6144-key chunk per tile)
 TILE = 24576
-BOUNDARIES = [4095, 4096, 4097, 6143, 6144, 6145, 16383, 16384, 16385, 24575, 24576, 24577, 2 * 24576 + 17]
+BOUNDARIES = [4095, 4096, 4097, 6143, 6144, 6145, 12287, 12288, 12289, 16384, 24575, 24576, 24577,
+              2 * 24576 + 17, 3 * 12288 + 5]
 
 
 def recs(keys):
