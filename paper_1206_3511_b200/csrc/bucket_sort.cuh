@@ -222,6 +222,7 @@ struct BucketDigitizer {
     __device__ __forceinline__ bool in_range(K key) const {
         return !check_range || static_cast<uint64_t>(key) <= bi.bound;
     }
+    __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }
     __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }
     __device__ __forceinline__ uint64_t super_bucket(K key) const {
         return bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> s_lo;
@@ -669,6 +670,7 @@ template <typename K>
 struct DestDigitizer {
     static constexpr int kDigits = 1;
     static constexpr bool kChecks = false;
+    __device__ __forceinline__ bool needs_range_check() const { return false; }
     static constexpr bool kCheapDigit = false;
     K split[kMaxParts - 1];
     int nsplit;

@@ -20,6 +20,8 @@
 //   K4 k_copy      only when no pass executes (sorted input): out = in.
 #pragma once
 
+#include <type_traits>
+
 #include "isort_common.cuh"
 
 namespace isort {
@@ -59,6 +61,7 @@ struct RadixDigitizer {
     static constexpr int kDigits = KeyTraits<K>::kDigits;
     static constexpr bool kChecks = false;
     static constexpr bool kCheapDigit = true;  // recompute instead of staging digits
+    __device__ __forceinline__ bool needs_range_check() const { return false; }
     __device__ __forceinline__ uint32_t shift_for(int pos) const { return 8u * static_cast<uint32_t>(pos); }
     // One PRMT per key: byte (sh / 8) of the key, zero-extended.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
@@ -98,79 +101,87 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     uint32_t desc = 0;
     unsigned long long first_bad = ~0ull;
 
-    auto visit = [&](K k, uint64_t idx) {
-        kmax = k > kmax ? k : kmax;
-        kmin = k < kmin ? k : kmin;
-        // Out-of-range keys are still counted (the digitizer clamps them) so the
-        // passes stay self-consistent; the host reports the first of them.
-        if (Dz::kChecks && !dz.in_range(k)) first_bad = idx < first_bad ? idx : first_bad;
-        uint32_t d[D];
-        dz.all_digits(k, d);
+    // The range check only exists where keys can exceed M: a template split keeps
+    // its compares out of the common loop.  Indices are 32-bit (n < 2^30).
+    auto run = [&](auto check_tag) {
+        constexpr bool CHECK = decltype(check_tag)::value;
+        auto visit = [&](K k, uint32_t idx) {
+            kmax = k > kmax ? k : kmax;
+            kmin = k < kmin ? k : kmin;
+            // Out-of-range keys are still counted (the digitizer clamps them) so the
+            // passes stay self-consistent; the host reports the first of them.
+            if (CHECK && !dz.in_range(k)) first_bad = idx < first_bad ? idx : first_bad;
+            uint32_t d[D];
+            dz.all_digits(k, d);
 #pragma unroll
-        for (int p = 0; p < D; ++p) atomicAdd(&uf_cnt[(p * kRadix + d[p]) * R + copy], 1u);
-    };
-
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * BLOCK;
-    constexpr int V = 4;  // 4 keys per thread-iteration
-    if (VEC) {
-        // Each warp streams U consecutive 512-byte blocks per step (U loads in
-        // flight per thread); the successor key for the sortedness check comes
-        // from the next lane, or the next block's lane 0.
-        const uint64_t nv = n / V;
-        constexpr int U = ISORT_UF_UNROLL;
-        const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (BLOCK / 32) * 32 * U;
-        for (uint64_t wb = (static_cast<uint64_t>(blockIdx.x) * (BLOCK / 32) + (threadIdx.x >> 5)) * 32 * U; wb < nv;
-             wb += wstride) {
-            K k[U][V];
+            for (int p = 0; p < D; ++p) atomicAdd(&uf_cnt[(p * kRadix + d[p]) * R + copy], 1u);
+        };
+        const uint32_t n32 = static_cast<uint32_t>(n);
+        const uint32_t stride = gridDim.x * BLOCK;
+        constexpr int V = 4;  // 4 keys per thread-iteration
+        if (VEC) {
+            // Each warp streams U consecutive 512-byte blocks per step (U loads in
+            // flight per thread); the successor key for the sortedness check comes
+            // from the next lane, or the next block's lane 0.
+            const uint32_t nv = n32 / V;
+            constexpr int U = ISORT_UF_UNROLL;
+            const uint32_t wstride = gridDim.x * (BLOCK / 32) * 32 * U;
+            for (uint32_t wb = (blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5)) * 32 * U; wb < nv; wb += wstride) {
+                K k[U][V];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t v = wb + static_cast<uint64_t>(u) * 32 + lane_id();
-                if (v < nv) {
-                    if (sizeof(K) == 4) {
-                        const uint4 q = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + v);
-                        k[u][0] = static_cast<K>(q.x);
-                        k[u][1] = static_cast<K>(q.y);
-                        k[u][2] = static_cast<K>(q.z);
-                        k[u][3] = static_cast<K>(q.w);
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t v = wb + u * 32 + lane_id();
+                    if (v < nv) {
+                        if (sizeof(K) == 4) {
+                            const uint4 q = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + v);
+                            k[u][0] = static_cast<K>(q.x);
+                            k[u][1] = static_cast<K>(q.y);
+                            k[u][2] = static_cast<K>(q.z);
+                            k[u][3] = static_cast<K>(q.w);
+                        } else {
+                            const uint4 a = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2ull * v);
+                            const uint4 b = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2ull * v + 1);
+                            k[u][0] = static_cast<K>((static_cast<uint64_t>(a.y) << 32) | a.x);
+                            k[u][1] = static_cast<K>((static_cast<uint64_t>(a.w) << 32) | a.z);
+                            k[u][2] = static_cast<K>((static_cast<uint64_t>(b.y) << 32) | b.x);
+                            k[u][3] = static_cast<K>((static_cast<uint64_t>(b.w) << 32) | b.z);
+                        }
                     } else {
-                        const uint4 a = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v);
-                        const uint4 b = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + 2 * v + 1);
-                        k[u][0] = static_cast<K>((static_cast<uint64_t>(a.y) << 32) | a.x);
-                        k[u][1] = static_cast<K>((static_cast<uint64_t>(a.w) << 32) | a.z);
-                        k[u][2] = static_cast<K>((static_cast<uint64_t>(b.y) << 32) | b.x);
-                        k[u][3] = static_cast<K>((static_cast<uint64_t>(b.w) << 32) | b.z);
+                        k[u][0] = 0;  // keep the shuffles below defined
                     }
-                } else {
-                    k[u][0] = 0;  // keep the shuffles below defined
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t v = wb + u * 32 + lane_id();
+                    K next = __shfl_down_sync(ISORT_FULL_MASK, k[u][0], 1);
+                    const K first_next_block = __shfl_sync(ISORT_FULL_MASK, k[u + 1 < U ? u + 1 : u][0], 0);
+                    if (lane_id() == 31) next = first_next_block;
+                    const bool from_mem = v + 1 >= nv || (lane_id() == 31 && u + 1 == U);
+                    if (v < nv) {
+                        if (from_mem) next = (v * V + V < n32) ? keys[v * V + V] : static_cast<K>(~static_cast<K>(0));
+                        desc += (k[u][0] > k[u][1]) + (k[u][1] > k[u][2]) + (k[u][2] > k[u][3]) + (k[u][3] > next);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) visit(k[u][j], v * V + j);
+                    }
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t v = wb + static_cast<uint64_t>(u) * 32 + lane_id();
-                K next = __shfl_down_sync(ISORT_FULL_MASK, k[u][0], 1);
-                const K first_next_block = __shfl_sync(ISORT_FULL_MASK, k[u + 1 < U ? u + 1 : u][0], 0);
-                if (lane_id() == 31) next = first_next_block;
-                const bool from_mem = v + 1 >= nv || (lane_id() == 31 && u + 1 == U);
-                if (v < nv) {
-                    if (from_mem) next = (v * V + V < n) ? keys[v * V + V] : static_cast<K>(~static_cast<K>(0));
-                    desc += (k[u][0] > k[u][1]) + (k[u][1] > k[u][2]) + (k[u][2] > k[u][3]) + (k[u][3] > next);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) visit(k[u][j], v * V + j);
-                }
+            for (uint32_t i = nv * V + blockIdx.x * BLOCK + threadIdx.x; i < n32; i += stride) {
+                const K k = keys[i];
+                if (i + 1 < n32) desc += (k > keys[i + 1]);
+                visit(k, i);
+            }
+        } else {
+            for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n32; i += stride) {
+                const K k = keys[i];
+                if (i + 1 < n32) desc += (k > keys[i + 1]);
+                visit(k, i);
             }
         }
-        for (uint64_t i = nv * V + static_cast<uint64_t>(blockIdx.x) * BLOCK + threadIdx.x; i < n; i += stride) {
-            const K k = keys[i];
-            if (i + 1 < n) desc += (k > keys[i + 1]);
-            visit(k, i);
-        }
-    } else {
-        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * BLOCK + threadIdx.x; i < n; i += stride) {
-            const K k = keys[i];
-            if (i + 1 < n) desc += (k > keys[i + 1]);
-            visit(k, i);
-        }
-    }
+    };
+    if (Dz::kChecks && dz.needs_range_check())
+        run(std::true_type{});
+    else
+        run(std::false_type{});
 
     // block reductions
     unsigned long long m = warp_max<unsigned long long>(static_cast<unsigned long long>(kmax));
