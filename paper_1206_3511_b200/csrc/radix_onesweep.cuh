@@ -266,11 +266,12 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
 //    lane-trials; re-verified at load time by k_selftest_atomic_order, with the
 //    match-based rank as the fallback).  So a key's stable rank is one atomicAdd.
 //  * The shared-memory pipe is the next wall: a random 4-byte access by 32 lanes
-//    costs ~3.5 bank wavefronts.  The pass therefore makes exactly two random
-//    shared accesses per key (rank atomic, staging store); counting uses
-//    lane-replicated counters (conflict-free).
+//    costs ~3.5 bank wavefronts.  Each key makes three random shared accesses
+//    (count atomic, rank atomic, staging store); everything else is sequential.
 //  * Decoupled look-back must walk (L2 latency x tile rate) predecessors; big
-//    tiles (NCHUNK chunks) keep that walk short.
+//    tiles keep that walk short (it costs <= 4% of the pass).
+//  * Big chunks pay: a 12,288-key chunk gives ~48-key runs per digit, so the
+//    scatter stores touch fewer partial lines and the counters cost less per key.
 //
 // Per tile (NCHUNK chunks of BLOCK*IPT keys, tile id by atomic ticket); warp w
 // always owns the same 32*IPT-key slice of every chunk, warp-striped (item i of
@@ -282,9 +283,10 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
 //              slot0(c, w, d) = sum_{d' < d} cnt_c(d') + sum_{w' < w} cnt(c, w', d)
 //   phase 2  per chunk: re-read keys (L2 hits), slot = atomicAdd(counter) (stable:
 //            lanes in order, items in program order), stage the key there (a
-//            digit-sorted chunk), then coalesced stores at out_base[c][d] + slot.
-// CTAs are small (256 threads, 4 per SM) and persistent; they take tiles by
-// atomic ticket, so every tile a CTA waits on is owned by a running CTA.
+//            digit-sorted chunk), then coalesced stores at out_base[c][d] + slot
+//            while the next chunk's keys load.
+// CTAs (512 threads, 2 per SM) are persistent and take tiles by atomic ticket,
+// so every tile a CTA waits on is owned by a running CTA.
 template <typename K, int BLOCK, int IPT, int NCHUNK, bool VALS, bool STAGE_DIGITS>
 struct OnesweepSmem {
     static constexpr int kWarps = BLOCK / 32;
