@@ -83,9 +83,13 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 #define ISORT_PASS_BLOCK 512
 #endif
 // One-sweep tile shape: BLOCK threads x IPT keys per chunk, CHUNKS chunks per
-// tile.  Large inputs use 4-chunk tiles (short look-back walks); inputs below
-// kSmallN use 1-chunk tiles so a few million keys still fill all SMs.
-constexpr uint64_t kSmallN = 4ull << 20;
+// tile.  Large inputs use 2 chunks of 24 keys per thread (DESIGN.md 3.1 has the
+// sweep); inputs below kSmallN use one 6,144-key chunk per tile so a few million
+// keys still fill all SMs (raising the threshold to 16M or 32M measured no gain).
+#ifndef ISORT_SMALL_N
+#define ISORT_SMALL_N (4ull << 20)
+#endif
+constexpr uint64_t kSmallN = ISORT_SMALL_N;
 
 #ifndef ISORT_PASS_CHUNKS
 #define ISORT_PASS_CHUNKS 2
