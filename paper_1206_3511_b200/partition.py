@@ -197,16 +197,17 @@ class PeerBuffers:
         self.lib = _lib.load()
         self.dist, self.device, self.capacity = dist, device, capacity
         g, me = dist.get_world_size(), dist.get_rank()
+        dev_index = device.index if device.index is not None else 0
         self.own, self.opened, handles = [], [], []
         ok = torch.ones(1, dtype=torch.int32, device=device)
         try:
             for _ in range(2):  # keys, payload
                 ptr = ctypes.c_void_p()
                 h = (ctypes.c_ubyte * 64)()
-                _lib.check(self.lib.isort_ipc_alloc(4 * max(capacity, 1), device.index, ctypes.byref(ptr), h))
+                _lib.check(self.lib.isort_ipc_alloc(4 * max(capacity, 1), dev_index, ctypes.byref(ptr), h))
                 self.own.append(int(ptr.value))
                 handles.append(bytes(h))
-        except _lib.IsortError:
+        except Exception:  # noqa: BLE001 - any local failure: every rank must still reach _agree
             ok.zero_()
             handles = [bytes(64), bytes(64)]
         self._agree(ok, "allocate")  # every rank takes the same branch before the next collective
@@ -225,12 +226,12 @@ class PeerBuffers:
                 for i in range(2):
                     ptr = ctypes.c_void_p()
                     hb = (ctypes.c_ubyte * 64).from_buffer_copy(raw[64 * i: 64 * (i + 1)])
-                    _lib.check(self.lib.isort_ipc_open(hb, device.index, ctypes.byref(ptr)))
+                    _lib.check(self.lib.isort_ipc_open(hb, dev_index, ctypes.byref(ptr)))
                     self.opened.append(int(ptr.value))
                     ptrs.append(int(ptr.value))
                 self.key_bases.append(ptrs[0])
                 self.val_bases.append(ptrs[1])
-        except _lib.IsortError:
+        except Exception:  # noqa: BLE001
             ok.zero_()
         self._agree(ok, "open")
 
@@ -241,7 +242,8 @@ class PeerBuffers:
             raise RuntimeError(f"PeerBuffers: some rank could not {what} its CUDA IPC buffers")
 
     def close(self):
-        torch.cuda.synchronize(self.device)
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
         if self.dist.get_world_size() > 1:
             self.dist.barrier()  # no peer still writes into our buffers
         for p in self.opened:

@@ -132,3 +132,28 @@ def test_fused_exchange_addresses():
     for d in range(3):  # the last source's run ends exactly at the destination's total
         last = fused_destinations(m, 2, bases, 4)[d] + 4 * m[2][d]
         assert last == bases[d] + 4 * recv_totals(m)[d]
+
+
+def _fused_fallback_worker(rank, world, port, out_dir):
+    """enable_fused on a box where CUDA IPC is unavailable: every rank must take
+    the same branch (agreement all-reduce) and keep the NCCL path -- no hang, no
+    half-enabled state."""
+    from paper_1206_3511_b200 import partition
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sorter = KeyRangeSorter(dist, TorchCpuOps())
+        keys = torch.arange(1000, dtype=torch.int32)
+        ok = partition.enable_fused(sorter, keys, "radix")
+        with open(os.path.join(out_dir, f"fb{rank}.txt"), "w") as f:
+            f.write(f"{int(ok)} {int(sorter.peers is None)}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_exchange_falls_back_on_every_rank(tmp_path):
+    world = 2
+    mp.spawn(_fused_fallback_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert (tmp_path / f"fb{r}.txt").read_text() == "0 1"
