@@ -148,6 +148,26 @@ int isort_radix_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n, int
 int isort_bucket_sort_host_u32(const uint32_t* in, uint32_t* out, uint64_t n,
                                uint64_t range_bound, int device);
 
+/* Asynchronous bucket sort: the same pipeline with no host synchronisation (so
+ * it can be captured in a CUDA graph).  The device writes the call's status to
+ * `status`, which must be host-pinned (cudaHostAlloc); after the stream passes
+ * that point, isort_bucket_finish_* reports a range error exactly as the
+ * synchronous call does, or re-sorts a span of oversized super-buckets (rare).
+ * `done` is set to 1 by the device when the other fields are final. */
+typedef struct isort_bucket_status {
+    uint64_t first_bad_not; /* ~index of the first key > range_bound; 0 if none */
+    uint64_t span_lo_not;   /* ~start of the oversized span (radix fallback) */
+    uint64_t span_hi;
+    uint32_t oversized;     /* non-constant oversized super-buckets */
+    uint32_t done;
+} isort_bucket_status;
+int isort_bucket_sort_u32_async(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                                uint32_t* vals_out, uint64_t n, uint64_t range_bound, int vals_mode, void* temp,
+                                size_t temp_bytes, isort_bucket_status* status, void* stream);
+int isort_bucket_finish_u32(const uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_out, uint64_t n,
+                            uint64_t range_bound, int vals_mode, void* temp, size_t temp_bytes,
+                            const isort_bucket_status* status, void* stream);
+
 /* Device batch of bucket_index (sort.hpp:42-48, sort.cpp:121-134): out[i] =
  * floor(bucket_count * keys[i] / (range_bound + 1)) with the exact 128-bit
  * semantics, or UINT64_MAX where keys[i] > range_bound.  ISORT_EINVAL when

@@ -62,6 +62,8 @@ SIGNATURES = {
     "isort_bucket_sort_host_u32": (_i32, [_vp, _vp, _u64, _u64, _i32]),
     "isort_is_sorted_u32": (_i32, [_vp, _u64, ctypes.POINTER(_i32), _vp]),
     "isort_bucket_index_u64": (_i32, [_vp, _vp, _u64, _u64, _u64, _vp]),
+    "isort_bucket_sort_u32_async": (_i32, [_vp, _vp, _vp, _vp, _u64, _u64, _i32, _vp, _sz, _vp, _vp]),
+    "isort_bucket_finish_u32": (_i32, [_vp, _vp, _vp, _u64, _u64, _i32, _vp, _sz, _vp, _vp]),
     "isort_partition_counts_u32": (_i32, [_vp, _u64, _vp, _i32, _vp, _vp, _sz, _vp]),
     "isort_partition_scatter_u32": (_i32, [_vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "isort_ipc_alloc": (_i32, [_sz, _i32, ctypes.POINTER(_vp), _vp]),

@@ -534,26 +534,88 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
     kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);
 }
 
-template <typename K, int MODE>
-int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
-                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s);
-
+// After the pipeline: report a range error like the reference, or re-sort the
+// span of non-constant oversized super-buckets with the radix pipeline.
 template <typename K>
-int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
-                       int vmode, void* temp, size_t temp_bytes, cudaStream_t s) {
-    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)))) {
-        case kPow2Narrow:
-            return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
-        case kMagicNarrow:
-            return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
-        default:
-            return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s);
+int bucket_finish_impl(const K* kin, K* kout, uint32_t* vout, uint64_t n, uint64_t bound, bool vals, void* temp,
+                       size_t temp_bytes, const isort_bucket_status* hs, cudaStream_t s) {
+    g_last_bad_index = ~0ull;
+    if (n == 0) return ISORT_OK;
+    if (!hs || !hs->done) return set_error(ISORT_EINVAL, "isort_bucket_finish: status not written by the device");
+    const BucketLayout L = bucket_layout<K>(n, vals);
+    if (!temp || temp_bytes < L.total)
+        return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
+    char* t = static_cast<char*>(temp);
+    auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
+    auto* lb = reinterpret_cast<uint32_t*>(t + L.r.lookback);
+    auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
+    auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
+    if (hs->first_bad_not != 0) {
+        const uint64_t idx = ~hs->first_bad_not;
+        K bad = 0;
+        ISORT_CUDA_TRY(cudaMemcpy(&bad, kin + idx, sizeof(K), cudaMemcpyDeviceToHost));
+        g_last_bad_index = idx;
+        return set_error(ISORT_EINVAL, "bucket_index: key %llu exceeds range bound %llu (sequence/spec mismatch)",
+                         (unsigned long long)bad, (unsigned long long)bound);
+    }
+    if (hs->oversized) {
+        const uint64_t lo = ~hs->span_lo_not, hi = hs->span_hi, m = hi - lo;
+        DevBuf tk, tv;
+        int rc;
+        if ((rc = tk.alloc(m * sizeof(K), s)) || (vals && (rc = tv.alloc(m * 4, s)))) return rc;
+        RadixDigitizer<K> rdz;
+        const uint32_t tiles_m = radix_layout<K>(m, vals).tiles;  // grid for the span, not for n
+        rc = vals ? launch_radix_pipeline<K, true>(kout + lo, tk.as<K>(), kalt + lo, vout + lo, tv.as<uint32_t>(),
+                                                   valt + lo, false, m, st, lb, tiles_m, rdz, true, true, s)
+                  : launch_radix_pipeline<K, false>(kout + lo, tk.as<K>(), kalt + lo, nullptr, nullptr, nullptr, false,
+                                                    m, st, lb, tiles_m, rdz, true, true, s);
+        if (rc) return rc;
+        k_copy_range<K><<<grid_for(m), 256, 0, s>>>(tk.as<K>(), kout + lo, vals ? tv.as<uint32_t>() : nullptr,
+                                                    vals ? vout + lo : nullptr, m);
+        launched();
+        prof_mark(s, "fallback");
+        ISORT_CUDA_TRY(cudaGetLastError());
+    }
+    return ISORT_OK;
+}
+
+// The status of an asynchronous bucket sort, written to host-pinned memory.
+__global__ void k_bucket_status(const RadixState* __restrict__ st, const BucketState* __restrict__ bst,
+                                isort_bucket_status* status) {
+    if (threadIdx.x == 0) {
+        status->first_bad_not = st->first_bad;
+        status->span_lo_not = bst->span_lo_not;
+        status->span_hi = bst->span_hi;
+        status->oversized = bst->oversized;
+        __threadfence_system();
+        status->done = 1;
     }
 }
 
 template <typename K, int MODE>
 int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
-                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s) {
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status);
+
+template <typename K>
+int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
+                       int vmode, void* temp, size_t temp_bytes, cudaStream_t s,
+                       isort_bucket_status* async_status = nullptr) {
+    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)))) {
+        case kPow2Narrow:
+            return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                    async_status);
+        case kMagicNarrow:
+            return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                     async_status);
+        default:
+            return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                              async_status);
+    }
+}
+
+template <typename K, int MODE>
+int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status) {
     static_assert(KeyTraits<K>::kDigits >= kBucketMaxDigits, "look-back sized for the bucket digit slots");
     g_last_bad_index = ~0ull;
     if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
@@ -591,38 +653,25 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     launched(1);
     ISORT_CUDA_TRY(cudaGetLastError());
 
+    if (async_status) {  // status to host memory from the device: no host sync, capturable
+        if (n == 0) return ISORT_OK;
+        k_bucket_status<<<1, 32, 0, s>>>(st, bst, async_status);
+        launched();
+        ISORT_CUDA_TRY(cudaGetLastError());
+        return ISORT_OK;
+    }
     // one small read-back: range error and oversized span
-    unsigned long long not_bad = 0;
+    isort_bucket_status hs{};
     BucketState hb{};
-    ISORT_CUDA_TRY(cudaMemcpyAsync(&not_bad, &st->first_bad, sizeof not_bad, cudaMemcpyDeviceToHost, s));
+    ISORT_CUDA_TRY(cudaMemcpyAsync(&hs.first_bad_not, &st->first_bad, sizeof hs.first_bad_not,
+                                   cudaMemcpyDeviceToHost, s));
     ISORT_CUDA_TRY(cudaMemcpyAsync(&hb, bst, sizeof hb, cudaMemcpyDeviceToHost, s));
     ISORT_CUDA_TRY(cudaStreamSynchronize(s));
-    if (not_bad != 0) {
-        const uint64_t idx = ~not_bad;
-        K bad = 0;
-        ISORT_CUDA_TRY(cudaMemcpy(&bad, kin + idx, sizeof(K), cudaMemcpyDeviceToHost));
-        g_last_bad_index = idx;
-        return set_error(ISORT_EINVAL, "bucket_index: key %llu exceeds range bound %llu (sequence/spec mismatch)",
-                         (unsigned long long)bad, (unsigned long long)bound);
-    }
-    if (hb.oversized) {
-        const uint64_t lo = ~hb.span_lo_not, hi = hb.span_hi, m = hi - lo;
-        DevBuf tk, tv;
-        if ((rc = tk.alloc(m * sizeof(K), s)) || (vals && (rc = tv.alloc(m * 4, s)))) return rc;
-        RadixDigitizer<K> rdz;
-        const uint32_t tiles_m = radix_layout<K>(m, vals).tiles;  // grid for the span, not for n
-        rc = vals ? launch_radix_pipeline<K, true>(kout + lo, tk.as<K>(), kalt + lo, vout + lo, tv.as<uint32_t>(),
-                                                   valt + lo, false, m, st, lb, tiles_m, rdz, true, true, s)
-                  : launch_radix_pipeline<K, false>(kout + lo, tk.as<K>(), kalt + lo, nullptr, nullptr, nullptr, false,
-                                                    m, st, lb, tiles_m, rdz, true, true, s);
-        if (rc) return rc;
-        k_copy_range<K><<<grid_for(m), 256, 0, s>>>(tk.as<K>(), kout + lo, vals ? tv.as<uint32_t>() : nullptr,
-                                                    vals ? vout + lo : nullptr, m);
-        launched();
-        prof_mark(s, "fallback");
-        ISORT_CUDA_TRY(cudaGetLastError());
-    }
-    return ISORT_OK;
+    hs.span_lo_not = hb.span_lo_not;
+    hs.span_hi = hb.span_hi;
+    hs.oversized = hb.oversized;
+    hs.done = 1;
+    return bucket_finish_impl<K>(kin, kout, vout, n, bound, vals, temp, temp_bytes, &hs, s);
 }
 
 template <typename K>
@@ -1028,6 +1077,22 @@ int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uin
                           void* stream) {
     return bucket_sort_device<uint64_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
                                         temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_bucket_sort_u32_async(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                                uint32_t* vals_out, uint64_t n, uint64_t range_bound, int vals_mode, void* temp,
+                                size_t temp_bytes, isort_bucket_status* status, void* stream) {
+    if (!status) return set_error(ISORT_EINVAL, "isort_bucket_sort_async: null status");
+    status->done = 0;
+    return bucket_sort_device<uint32_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
+                                        temp_bytes, static_cast<cudaStream_t>(stream), status);
+}
+
+int isort_bucket_finish_u32(const uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_out, uint64_t n,
+                            uint64_t range_bound, int vals_mode, void* temp, size_t temp_bytes,
+                            const isort_bucket_status* status, void* stream) {
+    return bucket_finish_impl<uint32_t>(keys_in, keys_out, vals_out, n, range_bound, vals_mode != ISORT_VALS_NONE,
+                                        temp, temp_bytes, status, static_cast<cudaStream_t>(stream));
 }
 
 size_t isort_partition_temp_bytes(uint64_t n, int key_bytes, int vals_mode) {

@@ -40,11 +40,14 @@ class Sorter:
     ``vals``: None (keys only), "iota" (payload = original position, generated on
     the device) or "load" (a payload tensor is passed to :meth:`__call__`).
 
-    ``graph=True`` (radix only, which never waits on the host): the first call
-    with a given input runs eagerly, the second captures the whole pipeline (state
-    reset, histogram, plan, passes, copy) into a CUDA graph, and later calls with
-    the same input and payload tensors replay it -- one launch instead of ~8,
-    which is what small, latency-bound sorts pay for.
+    ``graph=True``: the first call with a given input runs eagerly, the second
+    captures the whole pipeline (state reset, histogram, plan, passes, copy; for
+    the bucket sort also the segment sort and its status) into a CUDA graph, and
+    later calls with the same input and payload tensors replay it -- one launch
+    instead of ~10, which is what small, latency-bound sorts pay for.  The bucket
+    sort's status comes back through host-pinned memory
+    (isort_bucket_sort_u32_async) and is checked after the replay
+    (isort_bucket_finish_u32: range error, oversized fallback).
     """
 
     def __init__(self, n: int, key_bytes: int = 4, algorithm: str = RADIX, vals: str | None = None,
@@ -64,12 +67,14 @@ class Sorter:
         self.vals_out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)[:n] if vals else None
         self.temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
         self.temp_bytes = tb
-        self.graph = graph and algorithm == RADIX
+        self.graph = graph and (algorithm == RADIX or key_bytes == 4)
+        self._status = (torch.zeros(32, dtype=torch.uint8, pin_memory=True)
+                        if self.graph and algorithm == BUCKET else None)
         self._graph = None
         self._graph_key = None
         self.launches_per_call = None  # kernels in the captured pipeline
 
-    def __call__(self, keys: torch.Tensor, vals_in: torch.Tensor | None = None, stream=None):
+    def __call__(self, keys: torch.Tensor, vals_in: torch.Tensor | None = None, stream=None, eager: bool = False):
         _check_cuda(keys, "keys")
         if keys.numel() != self.n or _key_bytes(keys) != self.key_bytes:
             raise ValueError("keys do not match the Sorter's shape/width")
@@ -78,10 +83,13 @@ class Sorter:
                 raise ValueError("vals='load' needs a payload tensor of n elements")
             _check_cuda(vals_in, "vals")
         vin = vals_in.data_ptr() if (vals_in is not None and self.vmode == _lib.VALS_LOAD) else None
-        if self.graph and self.n > 0:
+        if self.graph and self.n > 0 and not eager:
             key = (keys.data_ptr(), vin)
             if self._graph is not None and self._graph_key == key:
+                if self._status is not None:
+                    self._status.zero_()
                 self._graph.replay()
+                self._finish(keys, stream)
                 return self.keys_out, self.vals_out
             if self._graph_key != key:  # first call with this input: eager (one-time library setup)
                 self._graph, self._graph_key = None, key
@@ -91,12 +99,37 @@ class Sorter:
             g = torch.cuda.CUDAGraph()
             l0 = lib.isort_launch_count()
             with torch.cuda.graph(g):
-                self._run(keys, vin, None)
+                if self._status is not None:
+                    self._run_async(keys, vin)
+                else:
+                    self._run(keys, vin, None)
             self.launches_per_call = int(lib.isort_launch_count() - l0)
             self._graph = g
+            if self._status is not None:
+                self._status.zero_()
             g.replay()
+            self._finish(keys, stream)
             return self.keys_out, self.vals_out
         return self._run(keys, vin, stream)
+
+    def _run_async(self, keys, vin):
+        lib = _lib.load()
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        vout = self.vals_out.data_ptr() if self.vals_out is not None else None
+        _lib.check(lib.isort_bucket_sort_u32_async(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n,
+                                                   int(self.range_bound), self.vmode, self.temp.data_ptr(),
+                                                   self.temp_bytes, self._status.data_ptr(), s))
+
+    def _finish(self, keys, stream):
+        """Bucket graphs: wait for the replay's status, then report / fall back."""
+        if self._status is None:
+            return
+        st = stream or torch.cuda.current_stream(self.device)
+        st.synchronize()
+        vout = self.vals_out.data_ptr() if self.vals_out is not None else None
+        _lib.check(_lib.load().isort_bucket_finish_u32(keys.data_ptr(), self.keys_out.data_ptr(), vout, self.n,
+                                                       int(self.range_bound), self.vmode, self.temp.data_ptr(),
+                                                       self.temp_bytes, self._status.data_ptr(), st.cuda_stream))
 
     def _run(self, keys, vin, stream):
         lib = _lib.load()

@@ -362,6 +362,35 @@ def test_radix_cuda_graph_replay(cuda, oracle, n):
     assert s._graph is not None and s.launches_per_call >= 3
 
 
+@pytest.mark.parametrize("n", [1000, 1_000_000, 5_000_003])
+def test_bucket_cuda_graph_replay(cuda, oracle, n):
+    """Sorter(graph=True) for the bucket sort: replays of the async pipeline,
+    status checked after each replay; range errors and the oversized fallback
+    still come out of the replay path."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(n + 1)
+    s = device.Sorter(n, 4, "bucket", "iota", range_bound=U32_MAX, graph=True)
+    buf = torch.empty(n, dtype=torch.int32, device="cuda")
+    for it in range(4):
+        k = (rng.integers(0, 1 << 32, size=n, dtype=np.uint64) if it != 2 else
+             rng.integers(0, 1 << 20, size=n, dtype=np.uint64)).astype(np.uint32)  # it 2: oversized span
+        buf.copy_(torch.from_numpy(k.view(np.int32)))
+        ko, vo = s(buf)
+        torch.cuda.synchronize()
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        assert np.array_equal(ko.cpu().numpy().view(np.uint32), want_k), it
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), want_i), it
+    assert s._graph is not None
+    bounded = device.Sorter(n, 4, "bucket", None, range_bound=1000, graph=True)
+    buf.copy_(torch.from_numpy(np.arange(n, dtype=np.int32) + 5))  # keys past 1000
+    for _ in range(3):  # eager, capture, replay: the range error every time
+        with pytest.raises(isort.InvalidArgument, match="exceeds range bound 1000"):
+            bounded(buf)
+
+
 def test_key_range_protocol_single_rank_gpu(cuda, oracle):
     """World size 1 through the same protocol object (no exchange), GPU kernels."""
     import torch
