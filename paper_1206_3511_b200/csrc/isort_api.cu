@@ -122,10 +122,10 @@ inline int pass_tile(uint64_t n) {
 // Upfront histogram replication (lane copies per bin): 64 KB of counters.
 template <int D>
 #ifndef ISORT_UF_REP
-#define ISORT_UF_REP 16
+#define ISORT_UF_REP 32
 #endif
 #ifndef ISORT_UF_BLOCK
-#define ISORT_UF_BLOCK 512
+#define ISORT_UF_BLOCK 1024
 #endif
 struct UpfrontCfg {
     static constexpr int kRep = D <= 4 ? ISORT_UF_REP : 8;
