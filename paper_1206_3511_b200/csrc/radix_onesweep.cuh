@@ -355,10 +355,16 @@ __device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ 
 }
 
 // L2 eviction policies: tile keys are read twice (count, then rank) so the first
-// read asks L2 to keep them; the re-read and the scattered stores are streaming.
+// read asks L2 to keep them (evict_last); the re-read and the scattered stores
+// use evict_normal (evict_first for them measured 1% slower).
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -588,8 +594,14 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     const uint32_t dsh = dz.shift_for(pos);
     uint32_t* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
     const bool vec = sizeof(K) == 4 && IPT % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
-    const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_stream = policy_evict_first();
+#ifndef ISORT_POL_KEEP
+#define ISORT_POL_KEEP policy_evict_last()
+#endif
+#ifndef ISORT_POL_STREAM
+#define ISORT_POL_STREAM policy_evict_normal()
+#endif
+    const uint64_t pol_keep = ISORT_POL_KEEP;
+    const uint64_t pol_stream = ISORT_POL_STREAM;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
