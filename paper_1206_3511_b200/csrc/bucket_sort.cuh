@@ -380,14 +380,15 @@ __device__ uint64_t warp_next_start(const K* __restrict__ keys, uint64_t n, uint
 }
 
 // Count / rank steps of seg_lsd for one warp's IPT x 32 positions; FULL: all in range.
-template <bool FULL, typename K, int IPT>
-__device__ __forceinline__ void seg_count(const K* ka, int obase, int len, K kmin, uint32_t shift, uint32_t mask,
-                                          uint32_t* wc, K (&kv)[IPT]) {
+template <bool FULL, typename K, int IPT, bool VALS>
+__device__ __forceinline__ void seg_count(const K* ka, const uint32_t* va, int obase, int len, K kmin, uint32_t shift,
+                                          uint32_t mask, uint32_t* wc, K (&kv)[IPT], uint32_t (&vv)[VALS ? IPT : 1]) {
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         const int o = obase + i * 32;
         if (FULL || o < len) {
             kv[i] = ka[o];
+            if (VALS) vv[i] = va[o];
             const uint32_t d = static_cast<uint32_t>((kv[i] - kmin) >> shift) & mask;
             atomicAdd(&wc[d >> 1], 1u << ((d & 1u) << 4));
         }
@@ -395,8 +396,9 @@ __device__ __forceinline__ void seg_count(const K* ka, int obase, int len, K kmi
 }
 
 template <bool FULL, typename K, int IPT, bool VALS>
-__device__ __forceinline__ void seg_rank(K* kb, const uint32_t* va, uint32_t* vb, int obase, int len, K kmin,
-                                         uint32_t shift, uint32_t mask, uint32_t* wc, const K (&kv)[IPT]) {
+__device__ __forceinline__ void seg_rank(K* kb, uint32_t* vb, int obase, int len, K kmin, uint32_t shift,
+                                         uint32_t mask, uint32_t* wc, const K (&kv)[IPT],
+                                         const uint32_t (&vv)[VALS ? IPT : 1]) {
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         const int o = obase + i * 32;
@@ -405,7 +407,7 @@ __device__ __forceinline__ void seg_rank(K* kb, const uint32_t* va, uint32_t* vb
             const uint32_t h = (d & 1u) << 4;
             const uint32_t slot = (atomicAdd(&wc[d >> 1], 1u << h) >> h) & 0xFFFFu;
             kb[slot] = kv[i];
-            if (VALS) vb[slot] = va[o];
+            if (VALS) vb[slot] = vv[i];
         }
     }
 }
@@ -432,14 +434,15 @@ __device__ __forceinline__ void block_minmax2(K& lo, K& hi, unsigned long long (
 }
 
 // Stable LSD sort of ka[0, len) (payload va) in shared memory by key - kmin,
-// `passes` r-bit digits (r <= SegDigits<BLOCK>::kBits); ka/kb (va/vb) swap each pass.
+// `passes` r-bit digits (r <= SegDigits<BLOCK>::kBits), in place: each pass
+// holds the stage in registers between its count and its scatter.
 // Rank primitive of the one-sweep pass: per-warp counters pre-scanned into slot
 // bases, slot = atomicAdd (lane-ordered, program-ordered => stable).  Warp w
 // owns positions [w*32*IPT, (w+1)*32*IPT); keys stay in registers between the
 // count and the rank step.
 template <typename K, int BLOCK, int IPT, bool VALS>
-__device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K*& ka, K*& kb, uint32_t*& va,
-                                        uint32_t*& vb, int len, K kmin, int passes, int r) {
+__device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K* ka, uint32_t* va, int len, K kmin,
+                                        int passes, int r) {
     constexpr int kWarps = BLOCK / 32;
     constexpr int kSegWords = SegDigits<BLOCK>::kWords;
     static_assert(BLOCK * IPT < 65536, "16-bit counters");
@@ -457,11 +460,12 @@ __device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K*& ka
         }
         __syncthreads();
         K kv[IPT];
+        uint32_t vv[VALS ? IPT : 1];
         const bool wfull = obase - static_cast<int>(lane) + 32 * IPT <= len;  // warp-uniform
         if (wfull)
-            seg_count<true, K, IPT>(ka, obase, len, kmin, shift, mask, wc, kv);
+            seg_count<true, K, IPT, VALS>(ka, va, obase, len, kmin, shift, mask, wc, kv, vv);
         else
-            seg_count<false, K, IPT>(ka, obase, len, kmin, shift, mask, wc, kv);
+            seg_count<false, K, IPT, VALS>(ka, va, obase, len, kmin, shift, mask, wc, kv, vv);
         __syncthreads();
         // thread t owns counter word t (digits 2t, 2t+1): totals over warps, scan, per-warp bases
         uint32_t lo = 0, hi = 0;
@@ -490,17 +494,12 @@ __device__ __forceinline__ void seg_lsd(SegSmem<K, BLOCK, IPT, VALS>& sm, K*& ka
             }
         }
         __syncthreads();
+        // in place: every key of the stage is in registers now
         if (wfull)
-            seg_rank<true, K, IPT, VALS>(kb, va, vb, obase, len, kmin, shift, mask, wc, kv);
+            seg_rank<true, K, IPT, VALS>(ka, va, obase, len, kmin, shift, mask, wc, kv, vv);
         else
-            seg_rank<false, K, IPT, VALS>(kb, va, vb, obase, len, kmin, shift, mask, wc, kv);
+            seg_rank<false, K, IPT, VALS>(ka, va, obase, len, kmin, shift, mask, wc, kv, vv);
         __syncthreads();
-        K* tk = ka;
-        ka = kb;
-        kb = tk;
-        uint32_t* tv = va;
-        va = vb;
-        vb = tv;
     }
 }
 
@@ -542,7 +541,9 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
         return seg_hi - p < static_cast<uint64_t>(kStage) ? static_cast<int>(seg_hi - p) : kStage;
     };
 
-    // Stage i+1 streams in (bulk copy) while stage i is written back.
+    // Stage i+1 streams in (bulk copy) while stage i is sorted and written back:
+    // the sort is in place, so the other buffer is free as soon as stage i's
+    // extent is known.
     int cur = 0;
     uint32_t phase = 0;
     BulkSplit ksp{}, vsp{};
@@ -591,10 +592,9 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
             if (e == pos + static_cast<uint64_t>(len)) {  // ends exactly with the stage
                 ls = len;
             } else {  // oversized: constant (nothing to do) or a span for the radix fallback
-                fence_proxy_async_smem();
-                __syncthreads();
-                cur ^= 1;
-                if (e < seg_hi) seg_issue<K, VALS>(keys, vals, e, stage_len(e), sm.buf[cur], sm.vbuf[cur], &sm.bar, ksp, vsp);
+                if (e < seg_hi)
+                    seg_issue<K, VALS>(keys, vals, e, stage_len(e), sm.buf[cur ^ 1], sm.vbuf[cur ^ 1], &sm.bar, ksp,
+                                       vsp);
                 kmin = static_cast<K>(~static_cast<K>(0));
                 kmax = 0;
                 for (uint64_t i = pos + tid; i < e; i += BLOCK) {
@@ -609,42 +609,33 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
                     atomicMax(&bst->span_hi, static_cast<unsigned long long>(e));
                 }
                 pos = e;
+                fence_proxy_async_smem();
                 __syncthreads();
+                cur ^= 1;
                 continue;
             }
         }
         const uint64_t next = pos + static_cast<uint64_t>(ls);
-        if (kmin == kmax) {  // one key value (or one key): arrival order is the answer, in place
-            fence_proxy_async_smem();
-            __syncthreads();
-            cur ^= 1;
-            if (next < seg_hi)
-                seg_issue<K, VALS>(keys, vals, next, stage_len(next), sm.buf[cur], sm.vbuf[cur], &sm.bar, ksp, vsp);
-            pos = next;
-            __syncthreads();
-            continue;
+        // the other buffer was last read by the previous write-back (before the
+        // end-of-iteration fence + barrier): the next stage can start landing now
+        if (next < seg_hi)
+            seg_issue<K, VALS>(keys, vals, next, stage_len(next), sm.buf[cur ^ 1], sm.vbuf[cur ^ 1], &sm.bar, ksp,
+                               vsp);
+        if (kmin != kmax) {  // else one key value (or one key): arrival order is the answer, in place
+            // ---- stable in-smem LSD sort of ka[0, ls) by (key - min)
+            const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
+            constexpr int kSegDigitBits = SegDigits<BLOCK>::kBits;
+            const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
+            seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, va, ls, kmin, passes, (bits + passes - 1) / passes);
+            for (int j = tid; j < ls; j += BLOCK) {
+                keys[pos + j] = ka[j];
+                if (VALS) vals[pos + j] = va[j];
+            }
         }
-
-        // ---- stable in-smem LSD sort of ka[0, ls) by (key - min), ping-pong with the other buffer
-        const int bits = 64 - __clzll(static_cast<unsigned long long>(kmax - kmin));
-        constexpr int kSegDigitBits = SegDigits<BLOCK>::kBits;
-        const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
-        K* kb = sm.buf[cur ^ 1];
-        uint32_t* vb = VALS ? sm.vbuf[cur ^ 1] : nullptr;
-        seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, kb, va, vb, ls, kmin, passes, (bits + passes - 1) / passes);
-        // the result is in ka; the next stage goes to the other buffer
-        const int tgt = ka == sm.buf[cur] + ksp.off ? cur ^ 1 : cur;
+        pos = next;
         fence_proxy_async_smem();
         __syncthreads();
-        if (next < seg_hi)
-            seg_issue<K, VALS>(keys, vals, next, stage_len(next), sm.buf[tgt], sm.vbuf[tgt], &sm.bar, ksp, vsp);
-        for (int j = tid; j < ls; j += BLOCK) {
-            keys[pos + j] = ka[j];
-            if (VALS) vals[pos + j] = va[j];
-        }
-        cur = tgt;
-        pos = next;
-        __syncthreads();
+        cur ^= 1;
     }
 }
 
