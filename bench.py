@@ -290,8 +290,13 @@ def main_ours(args):
     if world > 1:
         import torch.distributed as tdist
 
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("ISORT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # plumbing check only (several ranks may share one GPU): gloo + CPU-staged exchange
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            tdist.init_process_group(backend)
         dist = tdist
     else:
         torch.cuda.set_device(0)
@@ -387,6 +392,8 @@ def main_ours(args):
         else:
             line["gpu_launches"] = r["info"].get("launches")
             line["phases_ms"] = r["info"].get("phases")
+            line["exchange"] = r["info"].get("exchange")
+            line["max_over_mean_received"] = r["info"].get("max_over_mean_received")
             line["bucket"] = {"value": bvalue, "ms_per_step": b["ms"], "phases_ms": b["info"].get("phases")}
 
     # ------------------------------------------------ e2e through the host C-ABI

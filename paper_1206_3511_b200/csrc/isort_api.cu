@@ -804,22 +804,25 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
     ISORT_CUDA_TRY(cudaMemsetAsync(&st->tile_ticket[0], 0, sizeof(st->tile_ticket), s));
     auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
     const bool iota = vmode == ISORT_VALS_IOTA;
+    // the layout is the payload one (it covers both); the tile count must match the
+    // pass configuration actually launched (keys-only tiles are twice as long)
+    const uint32_t tiles = radix_layout<K>(n, vals).tiles;
     if (n < kSmallN) {
         if (vals)
             launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, 1>, true>(kin, nullptr, nullptr, vin, nullptr,
-                                                                              nullptr, iota, n, st, lb, L.tiles, dz, s,
+                                                                              nullptr, iota, n, st, lb, tiles, dz, s,
                                                                               scat);
         else
             launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, 1>, true>(
-                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
+                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, tiles, dz, s, scat);
     } else {
         if (vals)
             launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, ISORT_PASS_CHUNKS>, true>(kin, nullptr, nullptr, vin, nullptr,
-                                                                              nullptr, iota, n, st, lb, L.tiles, dz, s,
+                                                                              nullptr, iota, n, st, lb, tiles, dz, s,
                                                                               scat);
         else
             launch_passes<K, false, DestDigitizer<K>, PassCfg<K, false, ISORT_PASS_CHUNKS>, true>(
-                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz, s, scat);
+                kin, nullptr, nullptr, nullptr, nullptr, nullptr, false, n, st, lb, tiles, dz, s, scat);
     }
     launched(1);
     ISORT_CUDA_TRY(cudaGetLastError());

@@ -633,8 +633,8 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
         }
         __syncthreads();
         const uint32_t tile = sm.tile_id;
-        if (tile >= num_tiles) break;
         const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
+        if (tile >= num_tiles || tile_base >= n) break;  // (a tile count from another shape must not run past n)
         const uint32_t tile_len = static_cast<uint32_t>(n - tile_base < static_cast<uint64_t>(kTile)
                                                             ? n - tile_base : static_cast<uint64_t>(kTile));
 

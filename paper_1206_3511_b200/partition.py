@@ -156,6 +156,17 @@ class CudaOps:
         return a.elapsed_time(b)
 
 
+def _all_to_all(dist, out, inp, recv, send):
+    """all_to_all_single (NCCL over NVLink); under gloo (plumbing checks, CPU
+    tests) CUDA tensors are staged through host memory."""
+    if out.is_cuda and dist.get_backend() == "gloo":
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), output_split_sizes=recv, input_split_sizes=send)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, output_split_sizes=recv, input_split_sizes=send)
+
+
 def recv_totals(matrix: list[list[int]]) -> list[int]:
     """Keys each rank receives: column sums of the count matrix (row = source)."""
     g = len(matrix)
@@ -344,11 +355,11 @@ class KeyRangeSorter:
             send = [int(x) for x in counts.tolist()]
             recv = [int(allc[src][me].item()) for src in range(g)]
             out = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
-            self.dist.all_to_all_single(out, parted, output_split_sizes=recv, input_split_sizes=send)
+            _all_to_all(self.dist, out, parted, recv, send)
             vout = None
             if vals is not None:
                 vout = torch.empty(sum(recv), dtype=vals.dtype, device=vals.device)
-                self.dist.all_to_all_single(vout, pvals, output_split_sizes=recv, input_split_sizes=send)
+                _all_to_all(self.dist, vout, pvals, recv, send)
         else:
             out, vout = parted, pvals
         e3 = self.ops.event()

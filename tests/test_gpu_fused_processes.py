@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,world", [(3_000_017, 2), (1_000_003, 3), (777, 2)])
+@pytest.mark.parametrize("n,world", [(3_000_017, 2), (1_000_003, 3), (777, 2), (12_000_001, 2)])
 def test_fused_exchange_between_processes(n, world):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "two_rank_fused_check.py"), str(n), str(world)],
                        capture_output=True, text=True, timeout=600)

@@ -298,8 +298,9 @@ def test_partition_kernel_is_stable_grouping(cuda, parts):
         assert np.array_equal(ov.cpu().numpy(), v[order]), (parts, n)
 
 
-@pytest.mark.parametrize("parts", [2, 5, 8])
-def test_fused_partition_scatter_protocol(cuda, oracle, parts):
+@pytest.mark.parametrize("parts,n_extra,payload", [(2, 0, True), (5, 0, True), (8, 0, True),
+                                                   (3, 4_000_000, True), (4, 4_000_000, False)])
+def test_fused_partition_scatter_protocol(cuda, oracle, parts, n_extra, payload):
     """The fused exchange's kernels and address arithmetic on one GPU: `parts`
     simulated ranks run one after another (no kernel waits on another).  Each
     counts its shard, the count matrix gives every run's slot, and the partition
@@ -311,7 +312,7 @@ def test_fused_partition_scatter_protocol(cuda, oracle, parts):
     from paper_1206_3511_b200.partition import CudaOps, fused_destinations, recv_totals
 
     rng = np.random.default_rng(100 + parts)
-    n = 2_500_000 + parts * 7919
+    n = 2_500_000 + parts * 7919 + n_extra  # n_extra: past the small-n tile shape
     keys = oracle.mixture_u32(n, 40 + parts)
     pos = np.arange(n, dtype=np.int32)
     shards = np.array_split(np.arange(n), parts)
@@ -326,18 +327,24 @@ def test_fused_partition_scatter_protocol(cuda, oracle, parts):
     rv = [torch.full((t + 3,), -1, dtype=torch.int32, device="cuda") for t in totals]
     kb, vb = [t.data_ptr() for t in rk], [t.data_ptr() for t in rv]
     for r in range(parts):
-        ops[r].partition_scatter(tk[r], tv[r], spl, parts, fused_destinations(matrix, r, kb, 4),
-                                 fused_destinations(matrix, r, vb, 4))
+        ops[r].partition_scatter(tk[r], tv[r] if payload else None, spl, parts,
+                                 fused_destinations(matrix, r, kb, 4),
+                                 fused_destinations(matrix, r, vb, 4) if payload else None)
     torch.cuda.synchronize()
     got_k, got_v = [], []
     for d in range(parts):
-        assert (rk[d][totals[d]:] == -1).all() and (rv[d][totals[d]:] == -1).all(), "store past the slot"
-        k, v = device.radix_sort(rk[d][: totals[d]].contiguous(), vals=rv[d][: totals[d]].contiguous())
+        assert (rk[d][totals[d]:] == -1).all(), "store past the slot"
+        if payload:
+            assert (rv[d][totals[d]:] == -1).all(), "payload store past the slot"
+            k, v = device.radix_sort(rk[d][: totals[d]].contiguous(), vals=rv[d][: totals[d]].contiguous())
+            got_v.append(v.cpu().numpy())
+        else:
+            k, _ = device.radix_sort(rk[d][: totals[d]].contiguous())
         got_k.append(k.cpu().numpy().view(np.uint32))
-        got_v.append(v.cpu().numpy())
     want_k, want_i = oracle.sort_u32(keys, with_index=True)
     assert np.array_equal(np.concatenate(got_k), want_k)
-    assert np.array_equal(np.concatenate(got_v).astype(np.uint32), want_i)
+    if payload:
+        assert np.array_equal(np.concatenate(got_v).astype(np.uint32), want_i)
 
 
 @pytest.mark.parametrize("n", [1000, 1_000_000, 5_000_003])
