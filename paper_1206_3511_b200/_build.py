@@ -1,6 +1,6 @@
 """In-tree build of the engine (and of the parity checker under oracle/).
 
-* ``libisort.so``: every CUDA source in csrc/ compiled for sm_100a only
+* ``libisort.so``: every CUDA translation unit in csrc/ compiled for sm_100a only
   (``-gencode arch=compute_100a,code=sm_100a``), ``-lineinfo`` so ncu's source
   page maps to our code.  Built next to this file so it travels to the GPU box
   with the repo snapshot.
@@ -43,10 +43,11 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 
 def build_engine(force: bool = False, verbose: bool = False) -> str:
-    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+    units = sorted(glob.glob(os.path.join(CSRC, "*.cu")))  # translation units of libisort.so
+    sources = sorted(units + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
                      + [os.path.join(ROOT, "include", "isort.h")])
     if force or _stale(LIB, sources):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "isort_api.cu")]
+        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *units]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True, cwd=CSRC)
