@@ -1,0 +1,71 @@
+"""Randomised parity sweep on the GPU: many seeded (size, distribution, bound,
+payload, algorithm, graph) combinations against numpy's stable argsort.  Sizes
+straddle every tile shape (small-n 1-chunk tiles, 2-chunk tiles, payload tiles)
+and segment-stage boundary; distributions include runs, few distinct values,
+clustered and bucket-skewed keys."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+U32_MAX = (1 << 32) - 1
+
+
+def draw_keys(rng, n):
+    kind = rng.integers(0, 8)
+    if kind == 0:
+        k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+    elif kind == 1:  # few distinct values
+        k = rng.integers(0, int(rng.integers(1, 9)), size=n, dtype=np.uint64) * int(rng.integers(1, 1 << 28))
+    elif kind == 2:  # sorted runs
+        k = np.sort(rng.integers(0, 1 << 32, size=n, dtype=np.uint64))
+        cut = int(rng.integers(0, n + 1))
+        k = np.concatenate([k[cut:], k[:cut]])
+    elif kind == 3:  # descending
+        k = np.sort(rng.integers(0, 1 << 32, size=n, dtype=np.uint64))[::-1].copy()
+    elif kind == 4:  # clusters
+        k = (rng.integers(0, 40, size=n, dtype=np.uint64) * (1 << 26) + rng.integers(0, 1 << 10, size=n, dtype=np.uint64))
+    elif kind == 5:  # narrow range
+        k = rng.integers(0, 1 << int(rng.integers(1, 24)), size=n, dtype=np.uint64)
+    elif kind == 6:  # heavy duplicate + uniform
+        k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+        k[rng.random(n) < 0.4] = int(rng.integers(0, 1 << 32))
+    else:  # normal-ish
+        k = np.clip(np.rint(2.0**31 + 2.0**24 * rng.standard_normal(n)), 0, U32_MAX).astype(np.uint64)
+    return k.astype(np.uint32)
+
+
+SIZES = [1, 2, 100, 4095, 6144, 6145, 12288, 12289, 16383, 16385, 24576, 24577, 65537, 262_147,
+         (4 << 20) - 1, 4 << 20, (4 << 20) + 12289, 5_000_011]
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_parity_sweep(cuda, seed):
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(6):
+        n = int(SIZES[int(rng.integers(0, len(SIZES)))])
+        k = draw_keys(rng, n)
+        alg = "bucket" if rng.random() < 0.5 else "radix"
+        payload = ["iota", "load", None][int(rng.integers(0, 3))]
+        bound = U32_MAX if rng.random() < 0.6 else int(k.max()) + int(rng.integers(0, 1000))
+        graph = bool(rng.random() < 0.5)
+        s = device.Sorter(n, 4, alg, payload, range_bound=bound if alg == "bucket" else None, graph=graph)
+        tk = torch.from_numpy(k.view(np.int32)).cuda()
+        v = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        tv = torch.from_numpy(v.view(np.int32)).cuda() if payload == "load" else None
+        order = np.argsort(k, kind="stable")
+        for rep in range(3 if graph else 1):  # eager, capture + replay, replay
+            ko, vo = s(tk, tv)
+            torch.cuda.synchronize()
+            case = (seed, n, alg, payload, bound, graph, rep)
+            assert np.array_equal(ko.cpu().numpy().view(np.uint32), k[order]), case
+            if payload == "iota":
+                assert np.array_equal(vo.cpu().numpy().view(np.uint32), order.astype(np.uint32)), case
+            elif payload == "load":
+                assert np.array_equal(vo.cpu().numpy().view(np.uint32), v[order]), case
