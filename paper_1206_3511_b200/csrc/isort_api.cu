@@ -156,7 +156,7 @@ bool rank_fast_path_ok() {
 constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
 struct RadixLayout {
-    size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, scatter = 0, total = 0;
+    size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
     uint32_t tiles = 0;
 };
 
@@ -180,8 +180,6 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
     off += align_up(n * sizeof(K));
     L.vals_alt = off;
     if (vals) off += align_up(n * sizeof(uint32_t));
-    L.scatter = off;  // per-destination bases of a scatter pass
-    off += align_up(sizeof(ScatterTable));
     L.total = off;
     return L;
 }
@@ -223,7 +221,7 @@ int resident_per_sm(F* kernel, int block, size_t smem) {
 template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false>
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
                    uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
-                   const ScatterTable* scat = nullptr) {
+                   const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{}) {
     constexpr int D = Dz::kDigits;
     using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
     auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER>
@@ -783,9 +781,7 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
     }
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    auto* scat = reinterpret_cast<ScatterTable*>(t + L.scatter);
-    ISORT_CUDA_TRY(cudaMemcpyAsync(scat, &tbl, sizeof tbl, cudaMemcpyHostToDevice, s));
-    ISORT_CUDA_TRY(cudaStreamSynchronize(s));  // `tbl` is on this stack frame
+    const ScatterTable& scat = tbl;  // a kernel argument (by value): no copy, no host sync
     // the look-back words and the ticket of the (single) pass slot start from zero
     ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * sizeof(uint32_t), s));
     ISORT_CUDA_TRY(cudaMemsetAsync(&st->tile_ticket[0], 0, sizeof(st->tile_ticket), s));

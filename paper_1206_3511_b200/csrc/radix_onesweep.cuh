@@ -311,6 +311,11 @@ struct ScatterTable {
     unsigned long long key[kScatterMax];
     unsigned long long val[kScatterMax];
 };
+// Kernel argument: the table by value for a scatter pass (1 KB of parameters, no
+// copy or synchronisation on the host), nothing otherwise.
+struct NoScatter {};
+template <bool SCATTER>
+using ScatterArg = typename std::conditional<SCATTER, ScatterTable, NoScatter>::type;
 
 // Resident one-sweep CTAs per SM (the launch bound's minimum and the grid size).
 #ifndef ISORT_PASS_MINB
@@ -572,7 +577,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
-               uint32_t num_tiles, int slot, Dz dz, const ScatterTable* __restrict__ scat) {
+               uint32_t num_tiles, int slot, Dz dz, const ScatterArg<SCATTER> scat) {
     using Smem = OnesweepSmem<K, BLOCK, IPT, NCHUNK, VALS, !Dz::kCheapDigit>;
     constexpr int kWarps = Smem::kWarps;
     constexpr int kChunk = Smem::kChunk;
@@ -608,10 +613,12 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     const uint32_t lane = lane_id();
     if (tid < kRadix) sm.offs[tid] = st->offs[pos][tid];
     __shared__ unsigned long long s_kbase[SCATTER ? kScatterMax : 1], s_vbase[SCATTER ? kScatterMax : 1];
-    if (SCATTER && tid < kScatterMax) {  // per-digit base, shifted so that base + g addresses the run
-        const unsigned long long o = st->offs[pos][tid];
-        s_kbase[tid] = scat->key[tid] - o * sizeof(K);
-        if (VALS) s_vbase[tid] = scat->val[tid] - o * sizeof(uint32_t);
+    if constexpr (SCATTER) {
+        if (tid < kScatterMax) {  // per-digit base, shifted so that base + g addresses the run
+            const unsigned long long o = st->offs[pos][tid];
+            s_kbase[tid] = scat.key[tid] - o * sizeof(K);
+            if (VALS) s_vbase[tid] = scat.val[tid] - o * sizeof(uint32_t);
+        }
     }
 
 #ifdef ISORT_PHASE_TIMING
