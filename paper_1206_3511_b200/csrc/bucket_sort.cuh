@@ -295,6 +295,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// Bulk shared -> global copy (TMA store), tracked by the issuing thread's bulk group.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until this thread's bulk stores have read their shared-memory source (.read)
+// or have fully completed.
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+#ifndef ISORT_SEG_BULK_STORE
+#define ISORT_SEG_BULK_STORE 1
+#endif
 // Orders this thread's generic-proxy shared accesses before later async-proxy ones.
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -639,9 +653,34 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
             constexpr int kSegDigitBits = SegDigits<BLOCK>::kBits;
             const int passes = (bits + kSegDigitBits - 1) / kSegDigitBits;
             seg_lsd<K, BLOCK, IPT, VALS>(sm, ka, va, ls, kmin, passes, (bits + passes - 1) / passes);
-            for (int j = tid; j < ls; j += BLOCK) {
-                keys[pos + j] = ka[j];
-                if (VALS) vals[pos + j] = va[j];
+            if (ISORT_SEG_BULK_STORE && !ISORT_SEG_PREFETCH) {
+                // write-back by bulk copy (TMA store): the 16-byte-aligned interior of the
+                // sorted stage in one transfer, the head and tail by plain stores
+                fence_proxy_async_smem();  // the scatter's stores, visible to the async proxy
+                __syncthreads();
+                const BulkSplit kw = bulk_split(keys, pos, ls);
+                if (tid == 0 && kw.body)
+                    bulk_s2g(keys + pos + kw.head, ka + kw.head, static_cast<uint32_t>(kw.body * sizeof(K)));
+                if (tid < ls - kw.body) {
+                    const int j = tid < kw.head ? tid : kw.body + tid;
+                    keys[pos + j] = ka[j];
+                }
+                if (VALS) {
+                    const BulkSplit vw = bulk_split(vals, pos, ls);
+                    if (tid == 32 && vw.body)
+                        bulk_s2g(vals + pos + vw.head, va + vw.head, static_cast<uint32_t>(vw.body * 4));
+                    if (tid >= 64 && tid - 64 < ls - vw.body) {
+                        const int t = tid - 64;
+                        const int j = t < vw.head ? t : vw.body + t;
+                        vals[pos + j] = va[j];
+                    }
+                }
+                if (tid == 0 || tid == 32) bulk_wait_read();  // the buffer is reused by the next stage
+            } else {
+                for (int j = tid; j < ls; j += BLOCK) {
+                    keys[pos + j] = ka[j];
+                    if (VALS) vals[pos + j] = va[j];
+                }
             }
         }
         pos = next;
@@ -654,6 +693,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
             __syncthreads();
         }
     }
+    if (ISORT_SEG_BULK_STORE && (tid == 0 || tid == 32)) bulk_wait_all();  // stores complete before exit
 }
 
 template <typename K>
