@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -138,6 +139,10 @@ bool rank_fast_path_ok() {
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(g_rank_mu);
     if (g_rank_ok[dev & 63] != 0) return g_rank_ok[dev & 63] > 0;
+    if (const char* f = std::getenv("ISORT_FORCE_SAFE_RANK"); f && f[0] == '1') {  // tests of the fallback
+        g_rank_ok[dev & 63] = -1;
+        return false;
+    }
     uint32_t* d = nullptr;
     uint32_t bad = 1;
     if (cudaMalloc(&d, sizeof(uint32_t)) == cudaSuccess) {
@@ -633,13 +638,37 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
                                                     L.r.tiles, dz, true, true, s);
     if (rc) return rc;
     ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
-    if (vals)
-        launch_segments<K, BucketDigitizer<K, MODE>, true>(kout, vout, n, st, bst, dz, s);
-    else
-        launch_segments<K, BucketDigitizer<K, MODE>, false>(kout, nullptr, n, st, bst, dz, s);
-    prof_mark(s, "segments");
-    launched(1);
-    ISORT_CUDA_TRY(cudaGetLastError());
+    if (rank_fast_path_ok()) {
+        if (vals)
+            launch_segments<K, BucketDigitizer<K, MODE>, true>(kout, vout, n, st, bst, dz, s);
+        else
+            launch_segments<K, BucketDigitizer<K, MODE>, false>(kout, nullptr, n, st, bst, dz, s);
+        prof_mark(s, "segments");
+        launched(1);
+        ISORT_CUDA_TRY(cudaGetLastError());
+    } else {
+        // The segment sort ranks with lane-ordered shared atomics; without them, finish
+        // with the (match-based, stable) radix pipeline over the bucket-grouped keys --
+        // a stable sort of the whole array is the same result.  Runs only when the range
+        // check passed (the radix pipeline reuses the state).  Synchronises: not capturable.
+        unsigned long long not_bad = 0;
+        ISORT_CUDA_TRY(cudaMemcpyAsync(&not_bad, &st->first_bad, sizeof not_bad, cudaMemcpyDeviceToHost, s));
+        ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+        if (not_bad == 0) {
+            DevBuf tk, tv;
+            if ((rc = tk.alloc(n * sizeof(K), s)) || (vals && (rc = tv.alloc(n * 4, s)))) return rc;
+            RadixDigitizer<K> rdz;
+            rc = vals ? launch_radix_pipeline<K, true>(kout, tk.as<K>(), kalt, vout, tv.as<uint32_t>(), valt, false, n,
+                                                       st, lb, L.r.tiles, rdz, true, true, s)
+                      : launch_radix_pipeline<K, false>(kout, tk.as<K>(), kalt, nullptr, nullptr, nullptr, false, n, st,
+                                                        lb, L.r.tiles, rdz, true, true, s);
+            if (rc) return rc;
+            k_copy_range<K><<<grid_for(n), 256, 0, s>>>(tk.as<K>(), kout, vals ? tv.as<uint32_t>() : nullptr,
+                                                        vals ? vout : nullptr, n);
+            launched();
+            ISORT_CUDA_TRY(cudaGetLastError());
+        }  // else: the range error is still recorded in st and reported below
+    }
 
     if (async_status) {  // status to host memory from the device: no host sync, capturable
         if (n == 0) return ISORT_OK;

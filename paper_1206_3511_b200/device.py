@@ -67,7 +67,8 @@ class Sorter:
         self.vals_out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)[:n] if vals else None
         self.temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
         self.temp_bytes = tb
-        self.graph = graph and (algorithm == RADIX or key_bytes == 4)
+        # graphs need the lane-ordered rank (the fallback synchronises inside the bucket sort)
+        self.graph = graph and (algorithm == RADIX or key_bytes == 4) and lib.isort_rank_mode() != 0
         self._status = (torch.zeros(32, dtype=torch.uint8, pin_memory=True)
                         if self.graph and algorithm == BUCKET else None)
         self._graph = None
