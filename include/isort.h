@@ -114,6 +114,15 @@ int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uin
                           uint32_t* vals_out, uint64_t n, uint64_t range_bound, int vals_mode,
                           void* temp, size_t temp_bytes, void* stream);
 
+/* Bucket sort over the key span [range_lo, range_hi]: n buckets,
+ * b = floor(n * (key - range_lo) / (range_hi - range_lo + 1)).  Not a reference
+ * entry point (its ranges start at 0, where this equals isort_bucket_sort_u32);
+ * the multi-GPU sort's local step, where each rank holds one key range.  Keys
+ * outside the span fail with ISORT_EINVAL like a key above range_bound. */
+int isort_bucket_sort_span_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                               uint32_t* vals_out, uint64_t n, uint64_t range_lo, uint64_t range_hi,
+                               int vals_mode, void* temp, size_t temp_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Key-range partition (multi-GPU sort).  Not in the
  * reference (single-threaded); the engine's scale-out step.

@@ -35,22 +35,30 @@ namespace isort {
 
 // ------------------------------------------------------ bucket index
 // b(key) = floor(count * key / (M + 1)) exactly as bucket_index computes it
-// with unsigned __int128 (sort.cpp:131-133).
+// with unsigned __int128 (sort.cpp:131-133).  `base` generalises the range to
+// [base, M]: b = floor(count * (key - base) / (M - base + 1)).  The reference
+// API always has base = 0; the multi-GPU local sort (one key range per rank)
+// uses its range's lower end so the n buckets cover the keys it holds.
 struct BucketIndexer {
     uint64_t count;       // number of buckets (= n)
     uint64_t bound;       // M (inclusive range bound)
-    uint64_t div;         // M + 1 when it fits in 64 bits
+    uint64_t base;        // lower end of the range (0 for the reference API)
+    uint64_t span;        // M - base
+    uint64_t div;         // M - base + 1 when it fits in 64 bits
     uint64_t magic;       // floor((2^64 - 1) / div), general path
-    uint32_t pow2_shift;  // M + 1 == 2^pow2_shift (0..64), 255 otherwise
+    uint32_t pow2_shift;  // M - base + 1 == 2^pow2_shift (0..64), 255 otherwise
 
-    static BucketIndexer make(uint64_t count, uint64_t bound) {
+    static BucketIndexer make(uint64_t count, uint64_t bound, uint64_t base = 0) {
         BucketIndexer b{};
         b.count = count;
         b.bound = bound;
-        if (bound == ~0ull) {
+        b.base = base;
+        const uint64_t span = bound - base;
+        b.span = span;
+        if (span == ~0ull) {
             b.pow2_shift = 64;
         } else {
-            b.div = bound + 1;
+            b.div = span + 1;
             if ((b.div & (b.div - 1)) == 0) {
                 b.pow2_shift = static_cast<uint32_t>(__builtin_ctzll(b.div));
             } else {
@@ -65,6 +73,8 @@ struct BucketIndexer {
     // in bounds; k_upfront's range check reports them.
     __host__ __device__ __forceinline__ uint64_t bucket(uint64_t key) const {
         if (key > bound) return count - 1;
+        if (key < base) return 0;
+        key -= base;
 #ifdef __CUDA_ARCH__
         const uint64_t hi = __umul64hi(count, key);
 #else
@@ -89,7 +99,7 @@ struct BucketIndexer {
             }
             return q;
         }
-        // 128-by-64 division; the quotient is < count because key <= M.
+        // 128-by-64 division; the quotient is < count because key - base <= M - base.
         // Floating estimate, then exact integer correction.
         const double approx = (static_cast<double>(hi) * 18446744073709551616.0 + static_cast<double>(lo)) /
                               static_cast<double>(div);
@@ -135,8 +145,9 @@ enum BucketMode : int { kPow2Narrow = 0, kMagicNarrow = 1, kWide = 2 };
 template <int MODE>
 __device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t key) {
     if (MODE == kWide) return bi.bucket(key);
-    if (key > bi.bound) return bi.count - 1;
-    const uint64_t p = bi.count * key;  // exact: narrow modes guarantee < 2^64
+    const uint64_t k = key - bi.base;
+    if (k > bi.span) return key > bi.bound ? bi.count - 1 : 0;  // outside [base, M]: clamped
+    const uint64_t p = bi.count * k;  // exact: narrow modes guarantee < 2^64
     if (MODE == kPow2Narrow) return bi.pow2_shift >= 64 ? 0ull : p >> bi.pow2_shift;
     uint64_t q = __umul64hi(p, bi.magic);
     uint64_t r = p - q * bi.div;
@@ -148,11 +159,12 @@ __device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t 
     return q;
 }
 
-inline int choose_bucket_mode(uint64_t count, uint64_t bound, uint64_t key_max) {
-    const uint64_t kmax = bound < key_max ? bound : key_max;
+inline int choose_bucket_mode(uint64_t count, uint64_t bound, uint64_t key_max, uint64_t base = 0) {
+    const uint64_t kmax = (bound < key_max ? bound : key_max) - base;
     const bool narrow = static_cast<unsigned __int128>(count) * kmax < (static_cast<unsigned __int128>(1) << 64);
     if (!narrow) return kWide;
-    const bool pow2 = bound == ~0ull || ((bound + 1) & bound) == 0;
+    const uint64_t span = bound - base;
+    const bool pow2 = span == ~0ull || ((span + 1) & span) == 0;
     return pow2 ? kPow2Narrow : kMagicNarrow;
 }
 
@@ -174,11 +186,13 @@ struct BucketDigitizer {
     uint32_t tsh[kBucketMaxDigits];    // kPow2Narrow: log2(M + 1) + shift[p], capped at 64 (=> 0)
     uint32_t tshc[kBucketMaxDigits];   // min(tsh, 63) with dmask = 0 when tsh == 64: branch-free digits
     uint32_t dmask[kBucketMaxDigits];
-    uint32_t check_range;              // M < the largest key value: keys can be out of range
+    uint32_t check_range;              // [base, M] narrower than the key type: keys can be out of range
+    K kbase;                           // base in the key type (in-range keys are >= base)
 
-    static BucketDigitizer make(uint64_t n, uint64_t bound) {
+    static BucketDigitizer make(uint64_t n, uint64_t bound, uint64_t base = 0) {
         BucketDigitizer d{};
-        d.bi = BucketIndexer::make(n, bound);
+        d.bi = BucketIndexer::make(n, bound, base);
+        d.kbase = static_cast<K>(base);
         const uint32_t L = n > 1 ? 64 - __builtin_clzll(n - 1) : 0;  // bits of the largest bucket index
         uint32_t db = L > kSuperBucketBits ? (L - kSuperBucketBits + 7) / 8 : 0;
         if (db > kBucketMaxDigits) db = kBucketMaxDigits;
@@ -191,18 +205,20 @@ struct BucketDigitizer {
             d.tshc[p] = t < 64 ? t : 63;
             d.dmask[p] = t < 64 ? kRadix - 1 : 0;
         }
-        d.check_range = bound < static_cast<uint64_t>(~static_cast<K>(0)) ? 1u : 0u;
+        d.check_range = (bound < static_cast<uint64_t>(~static_cast<K>(0)) || base != 0) ? 1u : 0u;
         return d;
     }
+    // key - base in the key's width: u32 keys keep the 32x32->64 multiply
+    __device__ __forceinline__ uint64_t rel(K key) const { return static_cast<uint64_t>(static_cast<K>(key - kbase)); }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
         const uint32_t* t = MODE == kPow2Narrow ? tsh : shift;
         return pos == 0 ? t[0] : (pos == 1 ? t[1] : t[2]);
     }
-    // Digit of the bucket index.  Keys above M only reach here when the call is
-    // failing with a range error; their digits are then meaningless but < 256.
+    // Digit of the bucket index.  Keys outside [base, M] only reach here when the
+    // call is failing with a range error; their digits are then meaningless but < 256.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
         if (MODE == kPow2Narrow) {  // floor(n * key / 2^s) >> shift = (n * key) >> (s + shift); n < 2^32
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
             return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
         }
         return static_cast<uint32_t>(bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
@@ -210,7 +226,7 @@ struct BucketDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         if (MODE == kPow2Narrow) {
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
 #pragma unroll
             for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;
@@ -220,7 +236,7 @@ struct BucketDigitizer {
         for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const {
-        return !check_range || static_cast<uint64_t>(key) <= bi.bound;
+        return !check_range || static_cast<uint64_t>(key) - bi.base <= bi.span;
     }
     __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }
     __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }

@@ -531,7 +531,7 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
 // span of non-constant oversized super-buckets with the radix pipeline.
 template <typename K>
 int bucket_finish_impl(const K* kin, K* kout, uint32_t* vout, uint64_t n, uint64_t bound, bool vals, void* temp,
-                       size_t temp_bytes, const isort_bucket_status* hs, cudaStream_t s) {
+                       size_t temp_bytes, const isort_bucket_status* hs, cudaStream_t s, uint64_t base = 0) {
     g_last_bad_index = ~0ull;
     if (n == 0) return ISORT_OK;
     if (!hs || !hs->done) return set_error(ISORT_EINVAL, "isort_bucket_finish: status not written by the device");
@@ -548,6 +548,9 @@ int bucket_finish_impl(const K* kin, K* kout, uint32_t* vout, uint64_t n, uint64
         K bad = 0;
         ISORT_CUDA_TRY(cudaMemcpy(&bad, kin + idx, sizeof(K), cudaMemcpyDeviceToHost));
         g_last_bad_index = idx;
+        if (static_cast<uint64_t>(bad) < base)
+            return set_error(ISORT_EINVAL, "bucket_sort: key %llu below range base %llu",
+                             (unsigned long long)bad, (unsigned long long)base);
         return set_error(ISORT_EINVAL, "bucket_index: key %llu exceeds range bound %llu (sequence/spec mismatch)",
                          (unsigned long long)bad, (unsigned long long)bound);
     }
@@ -587,28 +590,33 @@ __global__ void k_bucket_status(const RadixState* __restrict__ st, const BucketS
 
 template <typename K, int MODE>
 int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
-                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status);
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status,
+                     uint64_t base);
 
 template <typename K>
 int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
                        int vmode, void* temp, size_t temp_bytes, cudaStream_t s,
-                       isort_bucket_status* async_status = nullptr) {
-    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)))) {
+                       isort_bucket_status* async_status = nullptr, uint64_t base = 0) {
+    if (base > bound)
+        return set_error(ISORT_EINVAL, "isort_bucket_sort: range base %llu above range bound %llu",
+                         (unsigned long long)base, (unsigned long long)bound);
+    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)), base)) {
         case kPow2Narrow:
             return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                                    async_status);
+                                                    async_status, base);
         case kMagicNarrow:
             return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                                     async_status);
+                                                     async_status, base);
         default:
             return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                              async_status);
+                                              async_status, base);
     }
 }
 
 template <typename K, int MODE>
 int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, uint64_t bound,
-                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status) {
+                     int vmode, void* temp, size_t temp_bytes, cudaStream_t s, isort_bucket_status* async_status,
+                     uint64_t base) {
     static_assert(KeyTraits<K>::kDigits >= kBucketMaxDigits, "look-back sized for the bucket digit slots");
     g_last_bad_index = ~0ull;
     if (vmode < ISORT_VALS_NONE || vmode > ISORT_VALS_IOTA)
@@ -629,7 +637,7 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
-    const BucketDigitizer<K, MODE> dz = BucketDigitizer<K, MODE>::make(n, bound);
+    const BucketDigitizer<K, MODE> dz = BucketDigitizer<K, MODE>::make(n, bound, base);
     const bool iota = vmode == ISORT_VALS_IOTA;
 
     int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, iota, n, st, lb, L.r.tiles, dz,
@@ -688,7 +696,7 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     hs.span_hi = hb.span_hi;
     hs.oversized = hb.oversized;
     hs.done = 1;
-    return bucket_finish_impl<K>(kin, kout, vout, n, bound, vals, temp, temp_bytes, &hs, s);
+    return bucket_finish_impl<K>(kin, kout, vout, n, bound, vals, temp, temp_bytes, &hs, s, base);
 }
 
 template <typename K>
@@ -932,6 +940,13 @@ int isort_bucket_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uin
                           void* stream) {
     return bucket_sort_device<uint64_t>(keys_in, keys_out, vals_in, vals_out, n, range_bound, vals_mode, temp,
                                         temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_bucket_sort_span_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                               uint32_t* vals_out, uint64_t n, uint64_t range_lo, uint64_t range_hi, int vals_mode,
+                               void* temp, size_t temp_bytes, void* stream) {
+    return bucket_sort_device<uint32_t>(keys_in, keys_out, vals_in, vals_out, n, range_hi, vals_mode, temp,
+                                        temp_bytes, static_cast<cudaStream_t>(stream), nullptr, range_lo);
 }
 
 int isort_bucket_sort_u32_async(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,

@@ -48,15 +48,23 @@ class Sorter:
     sort's status comes back through host-pinned memory
     (isort_bucket_sort_u32_async) and is checked after the replay
     (isort_bucket_finish_u32: range error, oversized fallback).
+
+    ``range_lo`` (bucket, u32 keys): the buckets cover [range_lo, range_bound]
+    instead of [0, range_bound] (isort_bucket_sort_span_u32) -- the multi-GPU
+    local sort, where a rank holds one key range.  Eager only.
     """
 
     def __init__(self, n: int, key_bytes: int = 4, algorithm: str = RADIX, vals: str | None = None,
-                 range_bound: int | None = None, device: torch.device | str = "cuda", graph: bool = False):
+                 range_bound: int | None = None, device: torch.device | str = "cuda", graph: bool = False,
+                 range_lo: int = 0):
         if algorithm not in (RADIX, BUCKET):
             raise ValueError(f"unknown algorithm {algorithm!r}")
         if algorithm == BUCKET and range_bound is None:
             range_bound = (1 << (8 * key_bytes)) - 1
+        if range_lo and (algorithm != BUCKET or key_bytes != 4):
+            raise ValueError("range_lo applies to the u32 bucket sort only")
         self.n, self.key_bytes, self.algorithm, self.range_bound = n, key_bytes, algorithm, range_bound
+        self.range_lo = int(range_lo)
         self.vmode = {None: _lib.VALS_NONE, "load": _lib.VALS_LOAD, "iota": _lib.VALS_IOTA}[vals]
         lib = _lib.load()
         tb = (lib.isort_radix_temp_bytes if algorithm == RADIX else lib.isort_bucket_temp_bytes)(
@@ -68,7 +76,8 @@ class Sorter:
         self.temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=self.device)
         self.temp_bytes = tb
         # graphs need the lane-ordered rank (the fallback synchronises inside the bucket sort)
-        self.graph = graph and (algorithm == RADIX or key_bytes == 4) and lib.isort_rank_mode() != 0
+        self.graph = (graph and (algorithm == RADIX or key_bytes == 4) and not self.range_lo
+                      and lib.isort_rank_mode() != 0)
         self._status = (torch.zeros(32, dtype=torch.uint8, pin_memory=True)
                         if self.graph and algorithm == BUCKET else None)
         self._graph = None
@@ -140,6 +149,10 @@ class Sorter:
             fn = lib.isort_radix_sort_u32 if self.key_bytes == 4 else lib.isort_radix_sort_u64
             rc = fn(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n, self.vmode,
                     self.temp.data_ptr(), self.temp_bytes, s)
+        elif self.range_lo:
+            rc = lib.isort_bucket_sort_span_u32(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n,
+                                                self.range_lo, int(self.range_bound), self.vmode,
+                                                self.temp.data_ptr(), self.temp_bytes, s)
         else:
             fn = lib.isort_bucket_sort_u32 if self.key_bytes == 4 else lib.isort_bucket_sort_u64
             rc = fn(keys.data_ptr(), self.keys_out.data_ptr(), vin, vout, self.n, int(self.range_bound),
@@ -156,10 +169,12 @@ def radix_sort(keys: torch.Tensor, vals: torch.Tensor | None = None, iota: bool 
     return k, v
 
 
-def bucket_sort(keys: torch.Tensor, range_bound: int, vals: torch.Tensor | None = None, iota: bool = False):
-    """One-shot device bucket sort over [0, range_bound]."""
+def bucket_sort(keys: torch.Tensor, range_bound: int, vals: torch.Tensor | None = None, iota: bool = False,
+                range_lo: int = 0):
+    """One-shot device bucket sort over [range_lo, range_bound] (the reference: range_lo = 0)."""
     mode = "load" if vals is not None else ("iota" if iota else None)
-    s = Sorter(keys.numel(), _key_bytes(keys), BUCKET, mode, range_bound=range_bound, device=keys.device)
+    s = Sorter(keys.numel(), _key_bytes(keys), BUCKET, mode, range_bound=range_bound, device=keys.device,
+               range_lo=range_lo)
     k, v = s(keys, vals)
     return k, v
 

@@ -140,7 +140,9 @@ class CudaOps:
         if keys.numel() == 0:
             return keys, vals
         if algorithm == "bucket":
-            k, v = device.bucket_sort(keys, hi, vals=vals)
+            # n buckets over this rank's key range [lo, hi], not [0, hi]: a rank
+            # high in the key space (or a narrow, dense range) keeps ~1 key per bucket
+            k, v = device.bucket_sort(keys, hi, vals=vals, range_lo=lo)
         else:
             k, v = device.radix_sort(keys, vals=vals)
         return k, v

@@ -219,6 +219,45 @@ def test_bucket_oversized_super_buckets(cuda, oracle):
     assert np.array_equal(got_i, want_i)
 
 
+@pytest.mark.parametrize("lo,hi", [(0, U32_MAX), (7 << 29, U32_MAX), (1 << 31, (1 << 31) + (1 << 24)),
+                                   (12345, 12345 + 1023), (1000, 1000), (5, U32_MAX - 1), (3, 10**8)])
+def test_bucket_span_sort(cuda, oracle, lo, hi):
+    """isort_bucket_sort_span_u32 (the multi-GPU local step): n buckets over
+    [lo, hi].  Any stable sort of the keys is the one correct output."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(lo ^ (hi & 0xFFFF))
+    for n in (10, 4097, 1_000_003):
+        u = rng.integers(lo, hi + 1, size=n, dtype=np.uint64)
+        c = np.clip(np.rint((lo + hi) / 2 + (hi - lo) / 64 * rng.standard_normal(n)), lo, hi).astype(np.uint64)
+        k = np.where(rng.integers(0, 2, size=n) > 0, u, c).astype(np.uint32)
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        t = torch.from_numpy(k.view(np.int32).copy()).cuda()
+        got_k, got_v = device.bucket_sort(t, hi, iota=True, range_lo=lo)
+        assert np.array_equal(got_k.cpu().numpy().view(np.uint32), want_k), (lo, hi, n)
+        assert np.array_equal(got_v.cpu().numpy().view(np.uint32), want_i), (lo, hi, n)
+        got_k, _ = device.bucket_sort(t, hi, range_lo=lo)  # keys only
+        assert np.array_equal(got_k.cpu().numpy().view(np.uint32), want_k), (lo, hi, n)
+
+
+def test_bucket_span_errors(cuda):
+    import torch
+
+    from paper_1206_3511_b200 import _lib, device
+
+    t = torch.from_numpy(np.array([500, 600, 499, 700], dtype=np.uint32).view(np.int32)).cuda()
+    with pytest.raises(isort.InvalidArgument, match="key 499 below range base 500"):
+        device.bucket_sort(t, 1000, range_lo=500)
+    assert _lib.load().isort_last_bad_index() == 2
+    with pytest.raises(isort.InvalidArgument, match="exceeds range bound 650"):
+        device.bucket_sort(torch.from_numpy(np.array([500, 651], dtype=np.uint32).view(np.int32)).cuda(), 650,
+                           range_lo=400)
+    with pytest.raises(isort.InvalidArgument, match="range base 700 above range bound 600"):
+        device.bucket_sort(t, 600, range_lo=700)
+
+
 @pytest.mark.parametrize("n", [5000, 8191, 8192, 8193, 20_000, 100_003, 1_000_003])
 def test_bucket_segment_kernel_paths(cuda, oracle, n):
     """The segment kernel's in-stage choices: sort by bucket + per-bucket
