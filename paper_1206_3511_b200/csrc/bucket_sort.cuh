@@ -137,18 +137,21 @@ struct BucketIndexer {
 };
 
 // Divisor kinds, chosen on the host once per call (compile-time in the kernels):
-//   kPow2Narrow   count * key < 2^64 and M + 1 = 2^s: one 64-bit multiply and a shift
-//   kMagicNarrow  count * key < 2^64: 64-bit magic reciprocal + <= 2 corrections
+//   kPow2Narrow   count * key < 2^64, base 0 and M + 1 = 2^s: one 64-bit multiply and a shift
+//   kMagicNarrow  count * (key - base) < 2^64: 64-bit magic reciprocal + <= 2 corrections
 //   kWide         general 128-by-64 division (BucketIndexer::bucket)
 enum BucketMode : int { kPow2Narrow = 0, kMagicNarrow = 1, kWide = 2 };
 
 template <int MODE>
 __device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t key) {
     if (MODE == kWide) return bi.bucket(key);
+    if (MODE == kPow2Narrow) {  // base == 0 (choose_bucket_mode)
+        if (key > bi.bound) return bi.count - 1;
+        return bi.pow2_shift >= 64 ? 0ull : (bi.count * key) >> bi.pow2_shift;
+    }
     const uint64_t k = key - bi.base;
     if (k > bi.span) return key > bi.bound ? bi.count - 1 : 0;  // outside [base, M]: clamped
     const uint64_t p = bi.count * k;  // exact: narrow modes guarantee < 2^64
-    if (MODE == kPow2Narrow) return bi.pow2_shift >= 64 ? 0ull : p >> bi.pow2_shift;
     uint64_t q = __umul64hi(p, bi.magic);
     uint64_t r = p - q * bi.div;
     if (r >= bi.div) {
@@ -164,7 +167,7 @@ inline int choose_bucket_mode(uint64_t count, uint64_t bound, uint64_t key_max, 
     const bool narrow = static_cast<unsigned __int128>(count) * kmax < (static_cast<unsigned __int128>(1) << 64);
     if (!narrow) return kWide;
     const uint64_t span = bound - base;
-    const bool pow2 = span == ~0ull || ((span + 1) & span) == 0;
+    const bool pow2 = base == 0 && (span == ~0ull || ((span + 1) & span) == 0);  // kPow2Narrow: base 0
     return pow2 ? kPow2Narrow : kMagicNarrow;
 }
 
@@ -187,12 +190,10 @@ struct BucketDigitizer {
     uint32_t tshc[kBucketMaxDigits];   // min(tsh, 63) with dmask = 0 when tsh == 64: branch-free digits
     uint32_t dmask[kBucketMaxDigits];
     uint32_t check_range;              // [base, M] narrower than the key type: keys can be out of range
-    K kbase;                           // base in the key type (in-range keys are >= base)
 
     static BucketDigitizer make(uint64_t n, uint64_t bound, uint64_t base = 0) {
         BucketDigitizer d{};
         d.bi = BucketIndexer::make(n, bound, base);
-        d.kbase = static_cast<K>(base);
         const uint32_t L = n > 1 ? 64 - __builtin_clzll(n - 1) : 0;  // bits of the largest bucket index
         uint32_t db = L > kSuperBucketBits ? (L - kSuperBucketBits + 7) / 8 : 0;
         if (db > kBucketMaxDigits) db = kBucketMaxDigits;
@@ -208,8 +209,6 @@ struct BucketDigitizer {
         d.check_range = (bound < static_cast<uint64_t>(~static_cast<K>(0)) || base != 0) ? 1u : 0u;
         return d;
     }
-    // key - base in the key's width: u32 keys keep the 32x32->64 multiply
-    __device__ __forceinline__ uint64_t rel(K key) const { return static_cast<uint64_t>(static_cast<K>(key - kbase)); }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
         const uint32_t* t = MODE == kPow2Narrow ? tsh : shift;
         return pos == 0 ? t[0] : (pos == 1 ? t[1] : t[2]);
@@ -218,7 +217,7 @@ struct BucketDigitizer {
     // call is failing with a range error; their digits are then meaningless but < 256.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
         if (MODE == kPow2Narrow) {  // floor(n * key / 2^s) >> shift = (n * key) >> (s + shift); n < 2^32
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
             return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
         }
         return static_cast<uint32_t>(bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
@@ -226,7 +225,7 @@ struct BucketDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         if (MODE == kPow2Narrow) {
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
 #pragma unroll
             for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;
@@ -236,6 +235,7 @@ struct BucketDigitizer {
         for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const {
+        if (MODE == kPow2Narrow) return !check_range || static_cast<uint64_t>(key) <= bi.bound;  // base 0
         return !check_range || static_cast<uint64_t>(key) - bi.base <= bi.span;
     }
     __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }

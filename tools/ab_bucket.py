@@ -18,6 +18,8 @@ ref = None
 for so in sys.argv[1:]:
     lib = ctypes.CDLL(os.path.abspath(so))
     for name, (res, args) in _lib.SIGNATURES.items():
+        if not hasattr(lib, name):  # older builds: entry points added since
+            continue
         f = getattr(lib, name)
         f.restype, f.argtypes = res, args
     tb = lib.isort_bucket_temp_bytes(n, 4, 0)
