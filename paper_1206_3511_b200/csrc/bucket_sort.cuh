@@ -285,9 +285,6 @@ struct SegSmem {
 };
 
 // ---- bulk (TMA) global -> shared copies completing on an mbarrier
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
@@ -311,22 +308,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
-// Bulk shared -> global copy (TMA store), tracked by the issuing thread's bulk group.
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// Wait until this thread's bulk stores have read their shared-memory source (.read)
-// or have fully completed.
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 #ifndef ISORT_SEG_BULK_STORE
 #define ISORT_SEG_BULK_STORE 1
 #endif
-// Orders this thread's generic-proxy shared accesses before later async-proxy ones.
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Split of src[pos, pos + len) into a head (up to the first 16-byte boundary),
 // a bulk-copyable interior of whole 16-byte blocks, and a tail.  Element j is

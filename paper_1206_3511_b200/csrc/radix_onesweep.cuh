@@ -287,17 +287,30 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
 //            while the next chunk's keys load.
 // CTAs (512 threads, 2 per SM) are persistent and take tiles by atomic ticket,
 // so every tile a CTA waits on is owned by a running CTA.
+// Experiment (off): write-out of a staged chunk by bulk copies (TMA stores), one
+// per digit run: each run is staged at a slot congruent to its global position
+// mod 4 (up to 3 pad slots per digit), so its 16-byte-aligned interior is one
+// cp.async.bulk.  Slower on B200: the runs average 48
+// keys, and the CTA waits for the copies to read the staging buffer before the
+// next chunk can be staged.
+#ifndef ISORT_PASS_BULK
+#define ISORT_PASS_BULK 0
+#endif
+constexpr int kStagePad = ISORT_PASS_BULK ? 4 * kRadix : 0;
+
 template <typename K, int BLOCK, int IPT, int NCHUNK, bool VALS, bool STAGE_DIGITS>
 struct OnesweepSmem {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kChunk = BLOCK * IPT;
     static constexpr int kTile = kChunk * NCHUNK;
+    static constexpr int kStage = kChunk + kStagePad;
     uint32_t cnt[NCHUNK][kWarps][kRadix];  // phase 1: counts; then chunk-local slot bases
     uint32_t out_base[NCHUNK][kRadix];     // global position = out_base[c][d] + slot
+    uint32_t run_start[ISORT_PASS_BULK ? NCHUNK : 1][kRadix];  // first staging slot of digit d's run
     uint32_t offs[kRadix];                 // pass digit offsets (from K2)
-    K keys[kChunk];
-    uint32_t vals[VALS ? kChunk : 1];
-    uint8_t digits[STAGE_DIGITS ? kChunk : 1];  // digit per staged key (expensive digitizers)
+    alignas(16) K keys[kStage];
+    alignas(16) uint32_t vals[VALS ? kStage : 1];
+    uint8_t digits[STAGE_DIGITS ? kStage : 1];  // digit per staged key (expensive digitizers)
     uint32_t tot_w[NCHUNK][kRadix / 32];
     uint32_t tile_id;
 };
@@ -508,6 +521,32 @@ __device__ __forceinline__ void chunk_write(Smem& sm, int c, K* __restrict__ dst
     }
 }
 
+// Write-out of chunk c by the thread of digit d: the run's 16-byte-aligned
+// interior by one bulk copy per array, the <= 3 + 3 keys around it by plain
+// stores.  Waits until the copies have read the staging buffer (it is reused
+// by the next chunk right after the caller's barrier).
+template <typename K, bool VALS, typename Smem>
+__device__ __forceinline__ void chunk_write_bulk(Smem& sm, int c, int d, K* __restrict__ dst,
+                                                 uint32_t* __restrict__ vdst, uint64_t pol) {
+    const uint32_t p = sm.run_start[c][d];
+    const uint32_t len = sm.cnt[c][Smem::kWarps - 1][d] - p;  // the last warp's counter ends the run
+    if (len == 0) return;
+    const uint32_t g = sm.out_base[c][d] + p;
+    auto put = [&](auto* gdst, const auto* sstage) {
+        using T = typename std::remove_cv<typename std::remove_pointer<decltype(sstage)>::type>::type;
+        constexpr uint32_t E = 16 / sizeof(T);
+        uint32_t head = (E - (g & (E - 1))) & (E - 1);
+        head = head < len ? head : len;
+        const uint32_t body = (len - head) & ~(E - 1);
+        if (body) bulk_s2g(gdst + g + head, sstage + p + head, body * static_cast<uint32_t>(sizeof(T)));
+        for (uint32_t i = 0; i < head; ++i) stg_hint(gdst + g + i, sstage[p + i], pol);
+        for (uint32_t i = head + body; i < len; ++i) stg_hint(gdst + g + i, sstage[p + i], pol);
+    };
+    put(dst, sm.keys);
+    if constexpr (VALS) put(vdst, sm.vals);
+    bulk_wait_read();
+}
+
 // Phase 1: per-(chunk, warp) digit counts of one tile (keys via L2, kept there
 // for phase 2).  AGG: the tile is expected to be made of sorted runs.
 template <bool AGG, typename K, typename Dz, int IPT, int NCHUNK, typename Smem>
@@ -579,6 +618,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
                int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
                uint32_t num_tiles, int slot, Dz dz, const ScatterArg<SCATTER> scat) {
     using Smem = OnesweepSmem<K, BLOCK, IPT, NCHUNK, VALS, !Dz::kCheapDigit>;
+    constexpr bool kBulkWrite = ISORT_PASS_BULK && !SCATTER;  // peer stores (SCATTER) stay per key
     constexpr int kWarps = Smem::kWarps;
     constexpr int kChunk = Smem::kChunk;
     constexpr int kTile = Smem::kTile;
@@ -695,6 +735,11 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
 #pragma unroll
                 for (int w = 0; w < kRadix / 32; ++w) pre += w < warp ? sm.tot_w[c][w] : 0u;
                 uint32_t base = pre + sc[c] - cc[c];  // chunk-local start of digit d
+                if (ISORT_PASS_BULK) {  // + 4d + (0..3): the run's slot = its global position mod 4
+                    base += 4u * static_cast<uint32_t>(d);
+                    base += (run - base) & 3u;
+                    sm.run_start[ISORT_PASS_BULK ? c : 0][d] = base;
+                }
                 sm.out_base[c][d] = run - base;
                 run += cc[c];
 #pragma unroll
@@ -739,6 +784,13 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
             else
                 chunk_rank<false, false, SAFE, K, Dz, IPT, VALS>(sm, c, key, val, valid, dsh, dz, warp, lane);
             if (c + 1 < NCHUNK && c0 + kChunk < tile_len) load(c + 1);  // in flight during the write-out
+            if constexpr (kBulkWrite) {
+                fence_proxy_async_smem();  // the staging stores, visible to the bulk copies
+                __syncthreads();
+                if (tid < kRadix) chunk_write_bulk<K, VALS>(sm, c, tid, dst, vdst, pol_stream);
+                __syncthreads();
+                continue;
+            }
             __syncthreads();
             if (full)
                 chunk_write<true, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, dst, vdst, valid, dsh, dz, pol_stream,
@@ -757,6 +809,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
 #endif
     }
     if (SCATTER) __threadfence_system();  // peer stores visible before the host-ordered barrier
+    if (kBulkWrite && tid < kRadix) bulk_wait_all();  // this CTA's bulk stores complete before it exits
 #ifdef ISORT_PHASE_TIMING
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
