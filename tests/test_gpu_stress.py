@@ -5,6 +5,8 @@ and segment-stage boundary; distributions include runs, few distinct values,
 clustered and bucket-skewed keys."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -41,7 +43,8 @@ SIZES = [1, 2, 100, 4095, 6144, 6145, 12288, 12289, 16383, 16385, 24576, 24577, 
          (4 << 20) - 1, 4 << 20, (4 << 20) + 12289, 5_000_011]
 
 
-@pytest.mark.parametrize("seed", range(24))
+# ISORT_STRESS_SEEDS widens the sweep for one-off runs (default 24 seeds)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ISORT_STRESS_SEEDS", "24"))))
 def test_random_parity_sweep(cuda, seed):
     import torch
 
@@ -54,8 +57,12 @@ def test_random_parity_sweep(cuda, seed):
         alg = "bucket" if rng.random() < 0.5 else "radix"
         payload = ["iota", "load", None][int(rng.integers(0, 3))]
         bound = U32_MAX if rng.random() < 0.6 else int(k.max()) + int(rng.integers(0, 1000))
-        graph = bool(rng.random() < 0.5)
-        s = device.Sorter(n, 4, alg, payload, range_bound=bound if alg == "bucket" else None, graph=graph)
+        # bucket sort over a span [lo, bound] (the multi-GPU local step) now and then
+        lo = int(k.min()) - int(rng.integers(0, 1000)) if alg == "bucket" and rng.random() < 0.25 else 0
+        lo = max(lo, 0)
+        graph = bool(rng.random() < 0.5) and lo == 0
+        s = device.Sorter(n, 4, alg, payload, range_bound=bound if alg == "bucket" else None, graph=graph,
+                          range_lo=lo)
         tk = torch.from_numpy(k.view(np.int32)).cuda()
         v = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
         tv = torch.from_numpy(v.view(np.int32)).cuda() if payload == "load" else None
@@ -63,7 +70,7 @@ def test_random_parity_sweep(cuda, seed):
         for rep in range(3 if graph else 1):  # eager, capture + replay, replay
             ko, vo = s(tk, tv)
             torch.cuda.synchronize()
-            case = (seed, n, alg, payload, bound, graph, rep)
+            case = (seed, n, alg, payload, bound, lo, graph, rep)
             assert np.array_equal(ko.cpu().numpy().view(np.uint32), k[order]), case
             if payload == "iota":
                 assert np.array_equal(vo.cpu().numpy().view(np.uint32), order.astype(np.uint32)), case
