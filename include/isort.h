@@ -184,6 +184,19 @@ int isort_bucket_finish_u32(const uint32_t* keys_in, uint32_t* keys_out, uint32_
 int isort_bucket_index_u64(const uint64_t* keys, uint64_t* out, uint64_t m, uint64_t bucket_count,
                            uint64_t range_bound, void* stream);
 
+/* One stable counting pass on device u32 keys by the general-base digit
+ * (key / base^digit_index) mod base.
+ * Replaces: intsort::counting_sort_by_digit(input, RadixPlan{base, digits},
+ *           digit_index) (sort.hpp:30-35, sort.cpp:77-110), with its errors:
+ *           base < 2, digit_index >= digits (ISORT_EINVAL, the reference's text).
+ * vals_mode as for the sorts (ISORT_VALS_IOTA: the source position of each key).
+ * Asynchronous on `stream`; temp from isort_counting_pass_temp_bytes(n). */
+size_t isort_counting_pass_temp_bytes(uint64_t n);
+int isort_counting_pass_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                            uint32_t* vals_out, uint64_t n, uint64_t base, uint32_t digits,
+                            uint32_t digit_index, int vals_mode, void* temp, size_t temp_bytes,
+                            void* stream);
+
 /* Device-side is_sorted (verify.hpp:12-13) over u32 keys: *result = 1/0. */
 int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* stream);
 

@@ -53,6 +53,8 @@ SIGNATURES = {
     "isort_bucket_sort_u32": (_i32, [_vp, _vp, _vp, _vp, _u64, _u64, _i32, _vp, _sz, _vp]),
     "isort_bucket_sort_u64": (_i32, [_vp, _vp, _vp, _vp, _u64, _u64, _i32, _vp, _sz, _vp]),
     "isort_bucket_sort_span_u32": (_i32, [_vp, _vp, _vp, _vp, _u64, _u64, _u64, _i32, _vp, _sz, _vp]),
+    "isort_counting_pass_temp_bytes": (_sz, [_u64]),
+    "isort_counting_pass_u32": (_i32, [_vp, _vp, _vp, _vp, _u64, _u64, _u32, _u32, _i32, _vp, _sz, _vp]),
     "isort_partition_temp_bytes": (_sz, [_u64, _i32, _i32]),
     "isort_partition_u32": (_i32, [_vp, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _sz, _vp]),
     "isort_radix_sort_records": (_i32, [_vp, _vp, _u64, _u64, _i32]),

@@ -463,6 +463,32 @@ __global__ void k_digit_keys(const isort_record* __restrict__ rec, uint64_t* __r
         d[i] = (rec[i].key / divisor) % base;
 }
 
+// Digit (key / divisor) mod base of u32 keys (counting_sort_by_digit, sort.cpp:95-97).
+__global__ void k_digit_u32(const uint32_t* __restrict__ keys, uint32_t* __restrict__ d, uint64_t n,
+                            uint64_t divisor, uint64_t base) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const bool pow2 = ((base & (base - 1)) == 0) && ((divisor & (divisor - 1)) == 0);
+    const uint32_t dsh = pow2 ? static_cast<uint32_t>(__ffsll(static_cast<long long>(divisor)) - 1) : 0u;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t k = keys[i];
+        d[i] = pow2 ? static_cast<uint32_t>(dsh < 64 ? (k >> dsh) & (base - 1) : 0)
+                    : static_cast<uint32_t>((k / divisor) % base);  // < 2^32: the quotient is <= k
+    }
+}
+
+// keys_out[i] = keys_in[idx[i]], and the payload (loaded, or the source position).
+__global__ void k_gather_pass_u32(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                  const uint32_t* __restrict__ idx, uint32_t* __restrict__ kout,
+                                  uint32_t* __restrict__ vout, uint64_t n, int vals_mode) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t j = idx[i];
+        kout[i] = kin[j];
+        if (vals_mode == ISORT_VALS_LOAD) vout[i] = vin[j];
+        else if (vals_mode == ISORT_VALS_IOTA) vout[i] = j;
+    }
+}
+
 __global__ void k_bucket_index(const uint64_t* __restrict__ keys, uint64_t* __restrict__ out, uint64_t m,
                                BucketIndexer bi) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -1130,6 +1156,51 @@ int isort_is_sorted_u32(const uint32_t* keys, uint64_t n, int* result, void* str
     ISORT_CUDA_TRY(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, s));
     ISORT_CUDA_TRY(cudaStreamSynchronize(s));
     *result = bad ? 0 : 1;
+    return ISORT_OK;
+}
+
+size_t isort_counting_pass_temp_bytes(uint64_t n) {
+    return 3 * align_up(n * 4) + radix_layout<uint32_t>(n, true).total;
+}
+
+int isort_counting_pass_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                            uint64_t n, uint64_t base, uint32_t digits, uint32_t digit_index, int vals_mode,
+                            void* temp, size_t temp_bytes, void* stream) {
+    g_last_bad_index = ~0ull;
+    if (base < 2) return set_error(ISORT_EINVAL, "counting_sort_by_digit: base must be >= 2");
+    if (digit_index >= digits)
+        return set_error(ISORT_EINVAL, "counting_sort_by_digit: digit_index %u out of range for a %u-digit plan",
+                         digit_index, digits);
+    if (vals_mode < ISORT_VALS_NONE || vals_mode > ISORT_VALS_IOTA)
+        return set_error(ISORT_EINVAL, "isort_counting_pass: bad vals_mode %d", vals_mode);
+    if (n == 0) return ISORT_OK;
+    if (n > kMaxLookbackN) return set_error(ISORT_ERANGE, "isort_counting_pass: n exceeds the per-call limit");
+    const bool vals = vals_mode != ISORT_VALS_NONE;
+    if (!keys_in || !keys_out || (vals && !vals_out) || (vals_mode == ISORT_VALS_LOAD && !vals_in))
+        return set_error(ISORT_EINVAL, "isort_counting_pass: null buffer");
+    const size_t need = isort_counting_pass_temp_bytes(n);
+    if (!temp || temp_bytes < need)
+        return set_error(ISORT_EINVAL, "isort_counting_pass: temp buffer too small (%zu < %zu)", temp_bytes, need);
+    uint64_t divisor = 1;  // pow_u64 (sort.cpp:28-34): the same wrap-around product
+    for (uint32_t i = 0; i < digit_index; ++i) divisor *= base;
+    if (divisor == 0)
+        return set_error(ISORT_EINVAL, "counting_sort_by_digit: base^%u overflows 64 bits", digit_index);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* t = static_cast<char*>(temp);
+    auto* dig = reinterpret_cast<uint32_t*>(t);
+    auto* dig_sorted = reinterpret_cast<uint32_t*>(t + align_up(n * 4));
+    auto* idx = reinterpret_cast<uint32_t*>(t + 2 * align_up(n * 4));
+    void* rtemp = t + 3 * align_up(n * 4);
+    // A counting pass is the stable sort by the digit: (digit, position) pairs
+    // through the radix pipeline (digits < 256 take one one-sweep pass), then a gather.
+    k_digit_u32<<<grid_for(n), 256, 0, s>>>(keys_in, dig, n, divisor, base);
+    launched();
+    int rc = radix_sort_device<uint32_t>(dig, dig_sorted, nullptr, idx, n, ISORT_VALS_IOTA, rtemp,
+                                         radix_layout<uint32_t>(n, true).total, s);
+    if (rc) return rc;
+    k_gather_pass_u32<<<grid_for(n), 256, 0, s>>>(keys_in, vals_in, idx, keys_out, vals_out, n, vals_mode);
+    launched();
+    ISORT_CUDA_TRY(cudaGetLastError());
     return ISORT_OK;
 }
 

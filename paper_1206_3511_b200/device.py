@@ -179,6 +179,30 @@ def bucket_sort(keys: torch.Tensor, range_bound: int, vals: torch.Tensor | None 
     return k, v
 
 
+def counting_pass(keys: torch.Tensor, base: int, digits: int, digit_index: int, vals: torch.Tensor | None = None,
+                  iota: bool = False):
+    """One stable device counting pass of u32 keys by digit (key / base^digit_index) mod base
+    (counting_sort_by_digit, sort.cpp:77-110).  Returns (keys, payload or None)."""
+    _check_cuda(keys, "keys")
+    if _key_bytes(keys) != 4:
+        raise TypeError("counting_pass: u32 keys")
+    n = keys.numel()
+    vmode = _lib.VALS_LOAD if vals is not None else (_lib.VALS_IOTA if iota else _lib.VALS_NONE)
+    if vals is not None:
+        _check_cuda(vals, "vals")
+    lib = _lib.load()
+    tb = lib.isort_counting_pass_temp_bytes(n)
+    temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=keys.device)
+    out = torch.empty_like(keys)
+    vout = torch.empty(n, dtype=torch.int32, device=keys.device) if vmode != _lib.VALS_NONE else None
+    s = torch.cuda.current_stream(keys.device).cuda_stream
+    _lib.check(lib.isort_counting_pass_u32(keys.data_ptr(), out.data_ptr(),
+                                           vals.data_ptr() if vals is not None else None,
+                                           vout.data_ptr() if vout is not None else None, n, int(base), int(digits),
+                                           int(digit_index), vmode, temp.data_ptr(), tb, s))
+    return out, vout
+
+
 def is_sorted_u32(keys: torch.Tensor) -> bool:
     import ctypes
 

@@ -219,6 +219,39 @@ def test_bucket_oversized_super_buckets(cuda, oracle):
     assert np.array_equal(got_i, want_i)
 
 
+@pytest.mark.parametrize("base,digits,idx", [(10, 10, 0), (10, 10, 3), (10, 10, 9), (256, 4, 1), (2, 32, 31),
+                                              (1000, 4, 2), (65536, 2, 1), ((1 << 32) + 5, 1, 0), (7, 12, 11)])
+def test_device_counting_pass(cuda, oracle, base, digits, idx):
+    """isort_counting_pass_u32 against the oracle's counting_sort_by_digit (sort.cpp:77-110)."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(base % 9973 + idx)
+    for n in (1, 1000, 100_003):
+        k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        want = oracle.counting_sort_by_digit(recs(k), base, digits, idx)
+        t = torch.from_numpy(k.view(np.int32).copy()).cuda()
+        ko, vo = device.counting_pass(t, base, digits, idx, iota=True)
+        assert np.array_equal(ko.cpu().numpy().view(np.uint32), want["key"].astype(np.uint32)), (base, idx, n)
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), want["tag"].astype(np.uint32)), (base, idx, n)
+        v = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        ko, vo = device.counting_pass(t, base, digits, idx, vals=torch.from_numpy(v.view(np.int32)).cuda())
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), v[want["tag"].astype(np.int64)]), (base, idx, n)
+
+
+def test_device_counting_pass_errors(cuda):
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    t = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(isort.InvalidArgument, match="base must be >= 2"):
+        device.counting_pass(t, 1, 3, 0)
+    with pytest.raises(isort.InvalidArgument, match="digit_index 3 out of range for a 3-digit plan"):
+        device.counting_pass(t, 10, 3, 3)
+
+
 @pytest.mark.parametrize("lo,hi", [(0, U32_MAX), (7 << 29, U32_MAX), (1 << 31, (1 << 31) + (1 << 24)),
                                    (12345, 12345 + 1023), (1000, 1000), (5, U32_MAX - 1), (3, 10**8)])
 def test_bucket_span_sort(cuda, oracle, lo, hi):
