@@ -77,7 +77,7 @@ inline void prof_mark(cudaStream_t s, const char* name) {
 #endif
 // One-sweep tile shape: BLOCK threads x IPT keys per chunk, CHUNKS chunks per
 // tile.  Large inputs use 2 chunks of 24 keys per thread (DESIGN.md 3.1 has the
-// sweep); inputs below kSmallN use one 6,144-key chunk per tile so a few million
+// sweep); inputs below kSmallN use one 8,192-key chunk per tile so a few million
 // keys still fill all SMs (raising the threshold to 16M or 32M measured no gain).
 #ifndef ISORT_SMALL_N
 #define ISORT_SMALL_N (4ull << 20)
@@ -99,8 +99,11 @@ struct PassCfg {
 #ifndef ISORT_PASS_IPT64
 #define ISORT_PASS_IPT64 12
 #endif
-    // keys per thread per chunk; the 1-chunk small-n tile keeps 12 (more tiles)
-    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? ISORT_PASS_IPT32V : (CHUNKS == 1 ? 12 : ISORT_PASS_IPT32))
+    // keys per thread per chunk; the 1-chunk small-n tile: 16 (1M keys: 51 us vs 57 with 12, 53 with 24)
+#ifndef ISORT_PASS_IPT_SMALL
+#define ISORT_PASS_IPT_SMALL 16
+#endif
+    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? ISORT_PASS_IPT32V : (CHUNKS == 1 ? ISORT_PASS_IPT_SMALL : ISORT_PASS_IPT32))
                                                : (VALS ? 6 : ISORT_PASS_IPT64);
     static constexpr int kChunks = CHUNKS;
     static constexpr int kTile = kBlock * kIpt * kChunks;

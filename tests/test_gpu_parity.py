@@ -18,9 +18,9 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 U32_MAX = (1 << 32) - 1
 # one-sweep geometry: chunk = 512 threads x IPT keys, tile = 2 chunks
 # (keys-only IPT 24: 12288 / 24576; with payload IPT 12: 6144 / 12288; below 4M keys
-# one 6144-key chunk per tile)
+# one chunk per tile: 8192 keys-only, 6144 with payload)
 TILE = 24576
-BOUNDARIES = [4095, 4096, 4097, 6143, 6144, 6145, 12287, 12288, 12289, 16384, 24575, 24576, 24577,
+BOUNDARIES = [4095, 4096, 4097, 6143, 6144, 6145, 8191, 8192, 8193, 12287, 12288, 12289, 16384, 24575, 24576, 24577,
               2 * 24576 + 17, 3 * 12288 + 5]
 
 
@@ -220,7 +220,7 @@ def test_bucket_oversized_super_buckets(cuda, oracle):
 
 
 @pytest.mark.parametrize("base,digits,idx", [(10, 10, 0), (10, 10, 3), (10, 10, 9), (256, 4, 1), (2, 32, 31),
-                                              (1000, 4, 2), (65536, 2, 1), ((1 << 32) + 5, 1, 0), (7, 12, 11)])
+                                              (1000, 4, 2), (65536, 2, 1), ((1 << 20) + 5, 2, 1), (7, 12, 11)])
 def test_device_counting_pass(cuda, oracle, base, digits, idx):
     """isort_counting_pass_u32 against the oracle's counting_sort_by_digit (sort.cpp:77-110)."""
     import torch

@@ -39,7 +39,7 @@ def draw_keys(rng, n):
     return k.astype(np.uint32)
 
 
-SIZES = [1, 2, 100, 4095, 6144, 6145, 12288, 12289, 16383, 16385, 24576, 24577, 65537, 262_147,
+SIZES = [1, 2, 100, 4095, 6144, 6145, 8192, 8193, 12288, 12289, 16383, 16385, 24576, 24577, 65537, 262_147,
          (4 << 20) - 1, 4 << 20, (4 << 20) + 12289, 5_000_011]
 
 
