@@ -4,7 +4,7 @@ partition kernel of each rank lands its runs in the other rank's receive buffer
 and that the rank-ordered result equals the global stable sort.  No kernel of
 one rank waits on a kernel of the other; only the host collectives synchronise.
 
-    python tools/two_rank_fused_check.py [n] [world]
+    python tools/two_rank_fused_check.py [n] [world] [radix|bucket]
 """
 import os
 import socket
@@ -17,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
-def worker(rank, world, port, n, out):
+def worker(rank, world, port, n, out, algorithm):
     from paper_1206_3511_b200 import inputs, partition
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -30,7 +30,7 @@ def worker(rank, world, port, n, out):
     pos = torch.from_numpy(sh.astype(np.int32)).to(dev)
     sorter = partition.KeyRangeSorter(dist, partition.CudaOps(dev))
     sorter.peers = partition.PeerBuffers(dist, dev, int(1.5 * k.numel()) + (1 << 16))
-    sk, sv, pt = sorter.sort(k, pos, algorithm="radix")
+    sk, sv, pt = sorter.sort(k, pos, algorithm=algorithm)
     torch.cuda.synchronize()
     np.save(os.path.join(out, f"k{rank}.npy"), sk.cpu().numpy().view(np.uint32))
     np.save(os.path.join(out, f"v{rank}.npy"), sv.cpu().numpy())
@@ -45,11 +45,12 @@ if __name__ == "__main__":
 
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 3_000_017
     world = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    algorithm = sys.argv[3] if len(sys.argv) > 3 else "radix"
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = tempfile.mkdtemp()
-    mp.spawn(worker, args=(world, port, n, out), nprocs=world, join=True)
+    mp.spawn(worker, args=(world, port, n, out, algorithm), nprocs=world, join=True)
     from paper_1206_3511_b200 import inputs
 
     keys = inputs.mixture_u32(n, 7)
@@ -58,5 +59,5 @@ if __name__ == "__main__":
     gv = np.concatenate([np.load(os.path.join(out, f"v{r}.npy")) for r in range(world)])
     paths = [open(os.path.join(out, f"path{r}.txt")).read() for r in range(world)]
     ok = np.array_equal(gk, keys[order]) and np.array_equal(gv.astype(np.int64), order)
-    print(f"paths={paths} n={n} bit-exact={ok}")
+    print(f"paths={paths} n={n} algorithm={algorithm} bit-exact={ok}")
     sys.exit(0 if ok and paths == ["fused"] * world else 1)
