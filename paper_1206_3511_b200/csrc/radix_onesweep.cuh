@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     __shared__ uint32_t red_desc[BLOCK / 32];
     for (int i = threadIdx.x; i < D * kRadix * R; i += BLOCK) uf_cnt[i] = 0;
     __syncthreads();
-    const uint32_t copy = lane_id() % R;
+    uint32_t* const my_cnt = uf_cnt + lane_id() % R;  // this lane's counter copy
 
     K kmax = 0;
     K kmin = static_cast<K>(~static_cast<K>(0));
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
             uint32_t d[D];
             dz.all_digits(k, d);
 #pragma unroll
-            for (int p = 0; p < D; ++p) atomicAdd(&uf_cnt[(p * kRadix + d[p]) * R + copy], 1u);
+            for (int p = 0; p < D; ++p) atomicAdd(my_cnt + (p * kRadix + d[p]) * R, 1u);
         };
         const uint32_t n32 = static_cast<uint32_t>(n);
         const uint32_t stride = gridDim.x * BLOCK;
@@ -126,8 +126,14 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
             const uint32_t nv = n32 / V;
             constexpr int U = ISORT_UF_UNROLL;
             const uint32_t wstride = gridDim.x * (BLOCK / 32) * 32 * U;
+            // successor of the last whole 4-key group: the scalar tail's first key, or none
+            const K tail_next = nv * V < n32 ? keys[nv * V] : static_cast<K>(~static_cast<K>(0));
             for (uint32_t wb = (blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5)) * 32 * U; wb < nv; wb += wstride) {
                 K k[U][V];
+                // lane 31's successor after the warp's last block: the next block's first key
+                const uint32_t vn = wb + U * 32;
+                const K step_next = (lane_id() == 31 && vn < nv) ? keys[static_cast<size_t>(vn) * V]
+                                                                  : static_cast<K>(~static_cast<K>(0));
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t v = wb + u * 32 + lane_id();
@@ -155,10 +161,9 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
                     const uint32_t v = wb + u * 32 + lane_id();
                     K next = __shfl_down_sync(ISORT_FULL_MASK, k[u][0], 1);
                     const K first_next_block = __shfl_sync(ISORT_FULL_MASK, k[u + 1 < U ? u + 1 : u][0], 0);
-                    if (lane_id() == 31) next = first_next_block;
-                    const bool from_mem = v + 1 >= nv || (lane_id() == 31 && u + 1 == U);
+                    if (lane_id() == 31) next = u + 1 < U ? first_next_block : step_next;
+                    if (v + 1 == nv) next = tail_next;
                     if (v < nv) {
-                        if (from_mem) next = (v * V + V < n32) ? keys[v * V + V] : static_cast<K>(~static_cast<K>(0));
                         desc += (k[u][0] > k[u][1]) + (k[u][1] > k[u][2]) + (k[u][2] > k[u][3]) + (k[u][3] > next);
 #pragma unroll
                         for (int j = 0; j < V; ++j) visit(k[u][j], v * V + j);

@@ -219,6 +219,23 @@ def test_bucket_oversized_super_buckets(cuda, oracle):
     assert np.array_equal(got_i, want_i)
 
 
+@pytest.mark.parametrize("n", [1000, 4099, 1_000_003, 5_000_001])
+def test_single_inversion_defeats_sorted_early_out(cuda, n):
+    """The histogram kernel's sortedness check (the sorted-input early-out) must see
+    one adjacent inversion anywhere: inside a 4-key group, across lanes, across a
+    warp's 512-byte blocks and steps, and in the scalar tail."""
+    base = np.arange(n, dtype=np.uint64) * 3 + 7
+    for p in sorted(q for q in {0, 2, 3, 4, 127, 128, 511, 512, 2047, 2048, n // 2, n - 5, n - 4, n - 3, n - 2}
+                    if q + 1 < n):
+        k = base.copy()
+        k[p], k[p + 1] = k[p + 1], k[p]
+        k = k.astype(np.uint32)
+        want = np.sort(k)
+        for alg in ("radix", "bucket"):
+            got, _ = dev_sort(k, alg, None, range_bound=(1 << 32) - 1 if alg == "bucket" else None)
+            assert np.array_equal(got, want), (n, p, alg)
+
+
 @pytest.mark.parametrize("base,digits,idx", [(10, 10, 0), (10, 10, 3), (10, 10, 9), (256, 4, 1), (2, 32, 31),
                                               (1000, 4, 2), (65536, 2, 1), ((1 << 20) + 5, 2, 1), (7, 12, 11)])
 def test_device_counting_pass(cuda, oracle, base, digits, idx):
