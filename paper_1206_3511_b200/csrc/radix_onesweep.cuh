@@ -40,7 +40,6 @@ struct RadixState {
     uint32_t hist[kMaxDigits][kRadix];  // K1
     uint32_t offs[kMaxDigits][kRadix];  // K2: exclusive scans
     unsigned long long max_key;         // K1
-    unsigned long long not_min_key;     // K1: ~min (so a zeroed word is the identity)
     unsigned long long first_bad;       // K1: ~(first index failing the range check)
     uint32_t descents;                  // K1: #i with key[i] > key[i+1]
     uint32_t n_active;                  // K2
@@ -90,14 +89,12 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     constexpr int D = Dz::kDigits;
     extern __shared__ __align__(16) uint32_t uf_cnt[];  // D * 256 * R
     __shared__ unsigned long long red_max[BLOCK / 32];
-    __shared__ unsigned long long red_nmin[BLOCK / 32];
     __shared__ uint32_t red_desc[BLOCK / 32];
     for (int i = threadIdx.x; i < D * kRadix * R; i += BLOCK) uf_cnt[i] = 0;
     __syncthreads();
     uint32_t* const my_cnt = uf_cnt + lane_id() % R;  // this lane's counter copy
 
     K kmax = 0;
-    K kmin = static_cast<K>(~static_cast<K>(0));
     uint32_t desc = 0;
     unsigned long long first_bad = ~0ull;
 
@@ -107,7 +104,6 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
         constexpr bool CHECK = decltype(check_tag)::value;
         auto visit = [&](K k, uint32_t idx) {
             kmax = k > kmax ? k : kmax;
-            kmin = k < kmin ? k : kmin;
             // Out-of-range keys are still counted (the digitizer clamps them) so the
             // passes stay self-consistent; the host reports the first of them.
             if (CHECK && !dz.in_range(k)) first_bad = idx < first_bad ? idx : first_bad;
@@ -190,13 +186,11 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
 
     // block reductions
     unsigned long long m = warp_max<unsigned long long>(static_cast<unsigned long long>(kmax));
-    unsigned long long nm = warp_max<unsigned long long>(~static_cast<unsigned long long>(kmin));
     uint32_t ds = warp_sum(desc);
     unsigned long long fb = warp_max<unsigned long long>(~first_bad);  // max of complements = min index
     const int w = threadIdx.x / 32;
     if (lane_id() == 0) {
         red_max[w] = m;
-        red_nmin[w] = nm;
         red_desc[w] = ds;
     }
     if (Dz::kChecks && lane_id() == 0 && fb != 0ull) atomicMax(&st->first_bad, fb);
@@ -204,14 +198,11 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     if (threadIdx.x < 32) {
         const int nw = BLOCK / 32;
         m = threadIdx.x < nw ? red_max[threadIdx.x] : 0ull;
-        nm = threadIdx.x < nw ? red_nmin[threadIdx.x] : 0ull;
         ds = threadIdx.x < nw ? red_desc[threadIdx.x] : 0u;
         m = warp_max<unsigned long long>(m);
-        nm = warp_max<unsigned long long>(nm);
         ds = warp_sum(ds);
         if (threadIdx.x == 0) {
             atomicMax(&st->max_key, m);
-            atomicMax(&st->not_min_key, nm);
             if (ds) atomicAdd(&st->descents, ds);
         }
     }
