@@ -46,7 +46,9 @@ struct BucketIndexer {
     uint64_t span;        // M - base
     uint64_t div;         // M - base + 1 when it fits in 64 bits
     uint64_t magic;       // floor((2^64 - 1) / div), general path
+    uint64_t qi, qf;      // count = qi * div + c', qf = ceil(2^64 * c' / div): b = k*qi + mulhi(k, qf)
     uint32_t pow2_shift;  // M - base + 1 == 2^pow2_shift (0..64), 255 otherwise
+    uint32_t div32;       // count and div both < 2^32: the 32-bit reciprocal path applies
 
     static BucketIndexer make(uint64_t count, uint64_t bound, uint64_t base = 0) {
         BucketIndexer b{};
@@ -59,12 +61,12 @@ struct BucketIndexer {
             b.pow2_shift = 64;
         } else {
             b.div = span + 1;
-            if ((b.div & (b.div - 1)) == 0) {
-                b.pow2_shift = static_cast<uint32_t>(__builtin_ctzll(b.div));
-            } else {
-                b.pow2_shift = 255;
-                b.magic = ~0ull / b.div;
-            }
+            b.magic = ~0ull / b.div;  // also for a power-of-two span: kMagicNarrow serves every base != 0
+            b.qi = count / b.div;
+            const unsigned __int128 num = static_cast<unsigned __int128>(count % b.div) << 64;
+            b.qf = static_cast<uint64_t>(num / b.div) + (num % b.div != 0 ? 1u : 0u);  // < 2^64: c' < div
+            b.div32 = b.div <= 0xFFFFFFFFull && count <= 0xFFFFFFFFull ? 1u : 0u;
+            b.pow2_shift = (b.div & (b.div - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctzll(b.div)) : 255u;
         }
         return b;
     }
@@ -180,7 +182,9 @@ struct BucketDigitizer {
     static constexpr bool kChecks = true;
     // narrow modes recompute the digit in the scatter phase (a multiply and a
     // shift are cheaper than staging digits through shared memory)
-    static constexpr bool kCheapDigit = MODE != kWide;
+    // narrow power-of-two bounds recompute the digit in the scatter phase; the
+    // other modes stage it (A/B on the B200: 1.94 vs 2.18 ms at 10^8, kMagicNarrow)
+    static constexpr bool kCheapDigit = MODE == kPow2Narrow;
     BucketIndexer bi;
     uint32_t shift[kBucketMaxDigits];  // digit p = (b >> shift[p]) & 255; unused: 63 (=> 0)
     uint32_t s_lo;                     // super-bucket = b >> s_lo
@@ -209,6 +213,25 @@ struct BucketDigitizer {
         d.check_range = (bound < static_cast<uint64_t>(~static_cast<K>(0)) || base != 0) ? 1u : 0u;
         return d;
     }
+    // Bucket index.  u32 keys with a general divisor: floor(n*k/div) = k*qi +
+    // floor(k*c'/div), and with qf = ceil(2^64 c'/div) = 2^64 c'/div + e (e < 1),
+    // floor(k*qf / 2^64) is exact: k*e/2^64 < 2^-32 <= 1/div cannot carry k*c'/div
+    // (whose fraction is <= (div-1)/div) past the next integer.  All in 32x32->64
+    // multiplies (n, div < 2^32; k <= span < div); a divisor of 2^32 or more takes
+    // the 64-bit reciprocal with corrections.
+    __device__ __forceinline__ uint64_t bidx(K key) const {
+        if constexpr (sizeof(K) == 4 && MODE == kMagicNarrow) {
+            if (!bi.div32) return bucket_of<MODE>(bi, static_cast<uint64_t>(key));
+            const uint64_t k64 = static_cast<uint64_t>(key) - bi.base;
+            if (k64 > bi.span) return key > bi.bound ? bi.count - 1 : 0;
+            const uint32_t k = static_cast<uint32_t>(k64);
+            const uint64_t lo = static_cast<uint64_t>(k) * static_cast<uint32_t>(bi.qf);
+            const uint64_t hi = static_cast<uint64_t>(k) * static_cast<uint32_t>(bi.qf >> 32);
+            return k * static_cast<uint32_t>(bi.qi) + static_cast<uint32_t>((hi + (lo >> 32)) >> 32);
+        } else {
+            return bucket_of<MODE>(bi, static_cast<uint64_t>(key));
+        }
+    }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
         const uint32_t* t = MODE == kPow2Narrow ? tsh : shift;
         return pos == 0 ? t[0] : (pos == 1 ? t[1] : t[2]);
@@ -220,7 +243,7 @@ struct BucketDigitizer {
             const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
             return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
         }
-        return static_cast<uint32_t>(bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> sh) & (kRadix - 1);
+        return static_cast<uint32_t>(bidx(key) >> sh) & (kRadix - 1);
     }
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
@@ -230,7 +253,7 @@ struct BucketDigitizer {
             for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;
         }
-        const uint64_t b = bucket_of<MODE>(bi, static_cast<uint64_t>(key));
+        const uint64_t b = bidx(key);
 #pragma unroll
         for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
@@ -239,9 +262,9 @@ struct BucketDigitizer {
         return !check_range || static_cast<uint64_t>(key) - bi.base <= bi.span;
     }
     __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }
-    __device__ __forceinline__ uint64_t bucket(K key) const { return bucket_of<MODE>(bi, static_cast<uint64_t>(key)); }
+    __device__ __forceinline__ uint64_t bucket(K key) const { return bidx(key); }
     __device__ __forceinline__ uint64_t super_bucket(K key) const {
-        return bucket_of<MODE>(bi, static_cast<uint64_t>(key)) >> s_lo;
+        return bidx(key) >> s_lo;
     }
 };
 
