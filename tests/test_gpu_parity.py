@@ -292,6 +292,37 @@ def test_bucket_span_sort(cuda, oracle, lo, hi):
         assert np.array_equal(got_k.cpu().numpy().view(np.uint32), want_k), (lo, hi, n)
 
 
+@pytest.mark.parametrize("lo,hi", [(7 << 29, U32_MAX), (1 << 30, (3 << 30) - 1), (12345, 12345 + (1 << 24) - 1),
+                                   (1000, 10**9 + 999), (0, 3 * 10**9)])
+def test_bucket_span_uniform_takes_no_fallback(cuda, lo, hi):
+    """Uniform keys over [lo, hi] spread ~1 key per bucket: every super-bucket fits a
+    stage, so the oversized-span radix fallback must not run (it did, silently, while
+    the reciprocal of power-of-two spans was missing -- correct output, 30x slower)."""
+    import ctypes
+
+    import torch
+
+    from paper_1206_3511_b200 import _lib, device
+
+    lib = _lib.load()
+    n = 1_000_003
+    k = np.random.default_rng(lo % 997).integers(lo, hi + 1, size=n, dtype=np.uint64).astype(np.uint32)
+    t = torch.from_numpy(k.view(np.int32).copy()).cuda()
+    s = device.Sorter(n, 4, "bucket", None, range_bound=hi, range_lo=lo)
+    s(t)
+    torch.cuda.synchronize()
+    assert lib.isort_profile_begin() == 0
+    s(t)
+    torch.cuda.synchronize()
+    ms = (ctypes.c_float * 512)()
+    names = ctypes.create_string_buffer(512 * 16)
+    cnt, na = ctypes.c_int(0), ctypes.c_int(0)
+    assert lib.isort_profile_end(ms, names, 16, 512, ctypes.byref(cnt), ctypes.byref(na)) == 0
+    phases = [names.raw[i * 16:(i + 1) * 16].split(b"\0")[0].decode() for i in range(cnt.value)]
+    assert "segments" in phases and "fallback" not in phases, phases
+    assert np.array_equal(s.keys_out.cpu().numpy().view(np.uint32), np.sort(k))
+
+
 def test_bucket_span_errors(cuda):
     import torch
 
