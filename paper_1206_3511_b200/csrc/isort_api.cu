@@ -354,7 +354,36 @@ int use_device(int device, cudaStream_t* out) {
     return ISORT_OK;
 }
 
-// RAII device allocation on the stream-ordered pool.
+// The library's stream-ordered memory pool, one per device.  Its release
+// threshold keeps up to ISORT_POOL_KEEP_BYTES (default 4 GiB) of freed
+// workspace mapped between calls: with the default pool (threshold 0) every
+// synchronising call hands the pages back and the next one maps them again,
+// which cost 5-45 ms per call for a 50 MB oversized-span fallback.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+int lib_pool(cudaMemPool_t* out) {
+    int dev = 0;
+    ISORT_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return set_error(ISORT_EINVAL, "device %d out of range", dev);
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        ISORT_CUDA_TRY(cudaMemPoolCreate(&pool, &props));
+        uint64_t keep = 4ull << 30;
+        if (const char* e = std::getenv("ISORT_POOL_KEEP_BYTES")) keep = std::strtoull(e, nullptr, 10);
+        ISORT_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        g_pools[dev] = pool;
+    }
+    *out = g_pools[dev];
+    return ISORT_OK;
+}
+
+// RAII device allocation on the library's stream-ordered pool.
 struct DevBuf {
     void* p = nullptr;
     cudaStream_t s = nullptr;
@@ -363,7 +392,9 @@ struct DevBuf {
     }
     int alloc(size_t bytes, cudaStream_t stream) {
         s = stream;
-        ISORT_CUDA_TRY(cudaMallocAsync(&p, bytes ? bytes : 16, stream));
+        cudaMemPool_t pool;
+        if (int rc = lib_pool(&pool)) return rc;
+        ISORT_CUDA_TRY(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream));
         return ISORT_OK;
     }
     template <typename T>
