@@ -53,6 +53,7 @@ class Oracle:
             "orc_generate": (_i32, [_i32, _u64, _i32, _u64, _u64, _i32, _u64, _dbl, _vp]),
             "orc_gen_uniform_u32": (None, [_u64, _u64, _u32, _vp]),
             "orc_gen_mixture_u32": (None, [_u64, _u64, _vp]),
+            "orc_gen_mixture_u32_range": (None, [_u64, _u64, _u64, _vp]),
             "orc_insertion_sort": (None, [_vp, _vp, _u64]),
             "orc_extract_digit": (_i32, [_u64, _u32, _u64, ctypes.POINTER(_u64)]),
             "orc_build_radix_plan": (_i32, [_vp, _u64, _u64, ctypes.POINTER(_u32)]),
@@ -107,9 +108,26 @@ class Oracle:
         self.lib.orc_gen_uniform_u32(n, seed, bits, _p(out))
         return out
 
-    def mixture_u32(self, n: int, seed: int = 42) -> np.ndarray:
+    def mixture_u32(self, n: int, seed: int = 42, threads: int | None = None) -> np.ndarray:
+        """Config-5 keys; large n is split over host threads (ctypes drops the GIL),
+        each writing its own index range -- the same values as one sequential call."""
         out = np.empty(n, dtype=np.uint32)
-        self.lib.orc_gen_mixture_u32(n, seed, _p(out))
+        threads = threads or (min(os.cpu_count() or 1, 32) if n >= (1 << 22) else 1)
+        if threads <= 1:
+            self.lib.orc_gen_mixture_u32(n, seed, _p(out))
+            return out
+        import threading
+
+        step = (n + threads - 1) // threads
+        def part(s):
+            c = min(step, n - s)
+            if c > 0:
+                self.lib.orc_gen_mixture_u32_range(s, c, seed, out.ctypes.data + 4 * s)
+        ths = [threading.Thread(target=part, args=(s,)) for s in range(0, n, step)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
         return out
 
     # sorting core (sort.cpp)

@@ -190,13 +190,13 @@ void orc_gen_uniform_u32(uint64_t n, uint64_t seed, uint32_t bits, uint32_t* out
  * mix(seed+(j+1)*gamma).  Component = top bit of x_{3i}; uniform ->
  * low 32 bits of x_{3i+1}; normal(2^31, 2^24) by Box-Muller on
  * x_{3i+1}, x_{3i+2}, rounded and clamped to [0, 2^32-1]. */
-void orc_gen_mixture_u32(uint64_t n, uint64_t seed, uint32_t* out) {
+void orc_gen_mixture_u32_range(uint64_t start, uint64_t count, uint64_t seed, uint32_t* out) {
     const double two_pi = 6.283185307179586476925286766559;
-    for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t i = start; i < start + count; ++i, ++out) {
         const uint64_t x0 = orc_mix64(seed + (3 * i + 1) * ORC_GAMMA);
         const uint64_t x1 = orc_mix64(seed + (3 * i + 2) * ORC_GAMMA);
         if (!(x0 >> 63)) {
-            out[i] = (uint32_t)x1;
+            *out = (uint32_t)x1;
         } else {
             const uint64_t x2 = orc_mix64(seed + (3 * i + 3) * ORC_GAMMA);
             const double u1 = 1.0 - (double)(x1 >> 11) * 0x1.0p-53; /* (0, 1] */
@@ -205,9 +205,13 @@ void orc_gen_mixture_u32(uint64_t n, uint64_t seed, uint32_t* out) {
             double v = llround(2147483648.0 + 16777216.0 * z);
             if (v < 0) v = 0;
             if (v > 4294967295.0) v = 4294967295.0;
-            out[i] = (uint32_t)v;
+            *out = (uint32_t)v;
         }
     }
+}
+
+void orc_gen_mixture_u32(uint64_t n, uint64_t seed, uint32_t* out) {
+    orc_gen_mixture_u32_range(0, n, seed, out);
 }
 
 /* ---------------------------------------------------------- sort core ---
