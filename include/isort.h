@@ -36,7 +36,7 @@ extern "C" {
 #define ISORT_OK 0
 #define ISORT_ENOMEM 12
 #define ISORT_EINVAL 22  /* reference: std::invalid_argument */
-#define ISORT_ERANGE 34  /* n beyond the engine's per-call limit (2^30 - 1 keys) */
+#define ISORT_ERANGE 34  /* n beyond the engine's per-call limit (2^32 - 1 keys, isort_max_keys()) */
 #define ISORT_EIO 5      /* reference: intsort::SequenceIoError (sequence files) */
 #define ISORT_ECUDA 1001
 #define ISORT_ENCCL 1002
@@ -76,6 +76,18 @@ uint64_t isort_launch_count(void);
  * atomics (lane order verified by the load-time self-test), 0 = the
  * __match_any_sync fallback (self-test failed), -1 = no device. */
 int isort_rank_mode(void);
+/* Select `device`, create the library's state on it and run the lane-order
+ * self-test the fast rank relies on.  Optional: the first sort does it lazily
+ * (on a private stream, with the thread's capture mode relaxed, so even a first
+ * call inside a CUDA-graph capture is safe); an explicit call keeps that
+ * one-time cost out of timed or captured regions. */
+int isort_init(int device);
+/* Host entry points take their device workspace from a library-owned,
+ * stream-ordered pool that keeps up to ISORT_POOL_KEEP_BYTES (env, default
+ * 4 GiB) of freed memory mapped between calls, so repeated calls do not remap
+ * pages.  isort_pool_trim releases all of it on `device` (the library also trims
+ * and retries once when an allocation fails). */
+int isort_pool_trim(int device);
 int isort_profile_begin(void);
 int isort_profile_end(float* ms, char* names, int names_stride, int max_phases, int* count,
                       int* n_active);
@@ -217,6 +229,14 @@ int isort_partition_counts_u32(const uint32_t* keys_in, uint64_t n, const uint32
 int isort_partition_scatter_u32(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n,
                                 const uint32_t* splitters, int parts, int vals_mode, void* const* key_dst,
                                 void* const* val_dst, void* temp, size_t temp_bytes, void* stream);
+/* Step 2 with a DEVICE-resident destination table (no host read of the count
+ * matrix before the launch): dst_table[d] = device address where this rank's run
+ * for destination d starts, dst_table[parts + d] = the same for the payload
+ * (ignored for ISORT_VALS_NONE).  The multi-GPU sort computes the table on the
+ * device from the all-gathered count matrix (paper_1206_3511_b200/partition.py). */
+int isort_partition_scatter_table_u32(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n,
+                                      const uint32_t* splitters, int parts, int vals_mode,
+                                      const uint64_t* dst_table, void* temp, size_t temp_bytes, void* stream);
 /* CUDA IPC for receive buffers: allocate + export a 64-byte handle, open a
  * peer's handle (peer access enabled lazily), close, free. */
 int isort_ipc_alloc(size_t bytes, int device, void** ptr, unsigned char* handle);

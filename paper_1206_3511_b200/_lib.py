@@ -43,6 +43,8 @@ SIGNATURES = {
     "isort_last_bad_index": (_u64, []),
     "isort_launch_count": (_u64, []),
     "isort_rank_mode": (_i32, []),
+    "isort_init": (_i32, [_i32]),
+    "isort_pool_trim": (_i32, [_i32]),
     "isort_profile_begin": (_i32, []),
     "isort_profile_end": (_i32, [ctypes.POINTER(ctypes.c_float), ctypes.c_char_p, _i32, _i32,
                                  ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
@@ -69,6 +71,7 @@ SIGNATURES = {
     "isort_bucket_finish_u32": (_i32, [_vp, _vp, _vp, _u64, _u64, _i32, _vp, _sz, _vp, _vp]),
     "isort_partition_counts_u32": (_i32, [_vp, _u64, _vp, _i32, _vp, _vp, _sz, _vp]),
     "isort_partition_scatter_u32": (_i32, [_vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "isort_partition_scatter_table_u32": (_i32, [_vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _sz, _vp]),
     "isort_ipc_alloc": (_i32, [_sz, _i32, ctypes.POINTER(_vp), _vp]),
     "isort_ipc_open": (_i32, [_vp, _i32, ctypes.POINTER(_vp)]),
     "isort_ipc_close": (_i32, [_vp]),

@@ -137,29 +137,74 @@ struct UpfrontCfg {
 std::mutex g_rank_mu;
 int g_rank_ok[64] = {0};  // 0 unknown, 1 verified, -1 failed
 
-bool rank_fast_path_ok() {
+// One run of the self-test on a private stream: 1 = lane order held, 0 = violations
+// counted, -1 = the test could not run (an API error; nothing is cached then).  The
+// thread's capture mode is relaxed for the duration, and every call is
+// stream-ordered on the private stream, so a first library call made while the
+// caller's stream is being captured into a CUDA graph neither fails nor
+// invalidates that capture.
+int run_rank_selftest() {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    cudaStream_t ts = nullptr;
+    uint32_t* d = nullptr;
+    uint32_t bad = ~0u;
+    int result = -1;
+    if (cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(uint32_t), ts) == cudaSuccess &&
+        cudaMemsetAsync(d, 0, sizeof(uint32_t), ts) == cudaSuccess) {
+        k_selftest_atomic_order<<<2 * sm_count(), 1024, 0, ts>>>(d, 0x5eedu);
+        if (cudaGetLastError() == cudaSuccess &&
+            cudaMemcpyAsync(&bad, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, ts) == cudaSuccess &&
+            cudaStreamSynchronize(ts) == cudaSuccess)
+            result = bad == 0 ? 1 : 0;
+    }
+    if (d) cudaFreeAsync(d, ts);
+    if (ts) {
+        cudaStreamSynchronize(ts);
+        cudaStreamDestroy(ts);
+    }
+    cudaGetLastError();  // a failed attempt leaves no sticky error for the caller's next check
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (result == 0)
+        std::fprintf(stderr, "isort: shared-atomic lane-order self-test failed (%u violations); "
+                             "using the __match_any_sync rank\n", bad);
+    return result;
+}
+
+// 1 verified, 0 failed (cached), -1 unknown (the test could not run; retried next call).
+int rank_state() {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(g_rank_mu);
-    if (g_rank_ok[dev & 63] != 0) return g_rank_ok[dev & 63] > 0;
+    int& c = g_rank_ok[dev & 63];
+    if (c != 0) return c > 0 ? 1 : 0;
     if (const char* f = std::getenv("ISORT_FORCE_SAFE_RANK"); f && f[0] == '1') {  // tests of the fallback
-        g_rank_ok[dev & 63] = -1;
-        return false;
+        c = -1;
+        return 0;
     }
-    uint32_t* d = nullptr;
-    uint32_t bad = 1;
-    if (cudaMalloc(&d, sizeof(uint32_t)) == cudaSuccess) {
-        cudaMemset(d, 0, sizeof(uint32_t));
-        k_selftest_atomic_order<<<2 * kNumSMs, 1024>>>(d, 0x5eedu);
-        if (cudaMemcpy(&bad, d, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) bad = 1;
-        cudaFree(d);
-    }
-    g_rank_ok[dev & 63] = bad == 0 ? 1 : -1;
-    if (bad)
-        std::fprintf(stderr, "isort: device %d failed the shared-atomic lane-order self-test (%u violations); "
-                             "using the __match_any_sync rank\n", dev, bad);
-    return bad == 0;
+    const int r = run_rank_selftest();
+    if (r >= 0) c = r ? 1 : -1;
+    return r;
 }
+bool rank_fast_path_ok() { return rank_state() == 1; }
+
+std::atomic<int> g_sm_count[64];
+
+}  // namespace isort
+
+int isort::sm_count() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = g_sm_count[dev & 63].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        g_sm_count[dev & 63].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+namespace isort {
 
 constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
@@ -183,7 +228,7 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
     L.state = off;
     off += align_up(sizeof(RadixState));
     L.lookback = off;
-    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * sizeof(uint32_t));
+    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * sizeof(LbWord));
     L.keys_alt = off;
     off += align_up(n * sizeof(K));
     L.vals_alt = off;
@@ -228,15 +273,15 @@ int resident_per_sm(F* kernel, int block, size_t smem) {
 
 template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false>
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
-                   uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
+                   uint64_t n, RadixState* st, LbWord* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
                    const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{}) {
     constexpr int D = Dz::kDigits;
     using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
     auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER>
                                      : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER>;
     set_max_smem_once(kern, sizeof(Smem));
-    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * kNumSMs) ? tiles
-                                                                                     : Cfg::kCtasPerSm * kNumSMs;
+    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * sm_count()) ? tiles
+                                                                                     : Cfg::kCtasPerSm * sm_count();
     for (int slot = 0; slot < D; ++slot) {
         kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
                                                         tiles, slot, dz, scat);
@@ -249,14 +294,14 @@ void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t
 // Histogram step of a pipeline: zero the state, K1 (all digit histograms, max,
 // sortedness, range check), K2 (scans + pass plan).
 template <typename K, typename Dz>
-int launch_histogram(const K* kin, uint64_t n, RadixState* st, uint32_t* lookback, uint32_t tiles, const Dz& dz,
+int launch_histogram(const K* kin, uint64_t n, RadixState* st, LbWord* lookback, uint32_t tiles, const Dz& dz,
                      int plan_flags, bool zero_state, cudaStream_t s) {
     constexpr int D = Dz::kDigits;
     prof_mark(s, "start");
     g_prof.st = st;
     if (zero_state) {
         const size_t bytes = reinterpret_cast<char*>(lookback) - reinterpret_cast<char*>(st) +
-                             static_cast<size_t>(D) * tiles * kRadix * sizeof(uint32_t);
+                             static_cast<size_t>(D) * tiles * kRadix * sizeof(LbWord);
         ISORT_CUDA_TRY(cudaMemsetAsync(st, 0, bytes, s));
         prof_mark(s, "memset");
     }
@@ -265,7 +310,7 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, uint32_t* lookbac
     const uint64_t want = (n + 4ull * kUpfrontBlock - 1) / (4ull * kUpfrontBlock);
     auto* k1 = vec ? k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, true> : k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, false>;
     set_max_smem_once(k1, UCfg::kSmem);
-    const uint64_t cap1 = static_cast<uint64_t>(resident_per_sm(k1, kUpfrontBlock, UCfg::kSmem)) * kNumSMs;
+    const uint64_t cap1 = static_cast<uint64_t>(resident_per_sm(k1, kUpfrontBlock, UCfg::kSmem)) * sm_count();
     const unsigned grid1 = static_cast<unsigned>(want < cap1 ? (want ? want : 1) : cap1);
     k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
     prof_mark(s, "upfront");
@@ -281,7 +326,7 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, uint32_t* lookbac
 // as ping-pong; the plan decides which passes run.
 template <typename K, bool VALS, typename Dz>
 int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
-                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, uint32_t* lookback,
+                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, LbWord* lookback,
                           uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
                           cudaStream_t s) {
     constexpr int D = Dz::kDigits;
@@ -296,7 +341,7 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
                                                         dz, s);
     launched(D);
     const uint64_t cblocks = (n + 4095) / 4096;
-    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 4ull * kNumSMs ? (cblocks ? cblocks : 1) : 4ull * kNumSMs), 512, 0, s>>>(
+    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 4ull * sm_count() ? (cblocks ? cblocks : 1) : 4ull * sm_count()), 512, 0, s>>>(
         kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
     prof_mark(s, "copy");
     ISORT_CUDA_TRY(cudaGetLastError());
@@ -320,7 +365,7 @@ int radix_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout
         return set_error(ISORT_EINVAL, "isort_radix_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
     RadixDigitizer<K> dz;
@@ -394,7 +439,14 @@ struct DevBuf {
         s = stream;
         cudaMemPool_t pool;
         if (int rc = lib_pool(&pool)) return rc;
-        ISORT_CUDA_TRY(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream));
+        if (cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream) != cudaSuccess) {
+            // out of memory with freed workspace still mapped: hand it back, retry once
+            cudaGetLastError();
+            p = nullptr;
+            cudaStreamSynchronize(stream);
+            cudaMemPoolTrimTo(pool, 0);
+            ISORT_CUDA_TRY(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, stream));
+        }
         return ISORT_OK;
     }
     template <typename T>
@@ -583,7 +635,7 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
     set_max_smem_once(kern, sizeof(Smem));
     const int per_sm = resident_per_sm(kern, kSegBlock, sizeof(Smem));
     const uint64_t want = (n + kSegBlock * kSegIpt / 2 - 1) / (kSegBlock * kSegIpt / 2);
-    const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * sm_count();
     kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);
 }
 
@@ -600,7 +652,7 @@ int bucket_finish_impl(const K* kin, K* kout, uint32_t* vout, uint64_t n, uint64
         return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
-    auto* lb = reinterpret_cast<uint32_t*>(t + L.r.lookback);
+    auto* lb = reinterpret_cast<LbWord*>(t + L.r.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     if (hs->first_bad_not != 0) {
@@ -693,7 +745,7 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
         return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
-    auto* lb = reinterpret_cast<uint32_t*>(t + L.r.lookback);
+    auto* lb = reinterpret_cast<LbWord*>(t + L.r.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
@@ -706,7 +758,15 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
                                                     L.r.tiles, dz, true, true, s);
     if (rc) return rc;
     ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
-    if (rank_fast_path_ok()) {
+    const int rank_ok = rank_state();
+    if (rank_ok < 0) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs != cudaStreamCaptureStatusNone)
+            return set_error(ISORT_ECUDA, "isort_bucket_sort: the lane-order self-test could not run; "
+                                          "call isort_init() outside stream capture first");
+    }
+    if (rank_ok == 1) {
         if (vals)
             launch_segments<K, BucketDigitizer<K, MODE>, true>(kout, vout, n, st, bst, dz, s);
         else
@@ -796,7 +856,7 @@ int partition_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
         return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
     int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, vmode == ISORT_VALS_IOTA, n, st,
@@ -846,7 +906,7 @@ int partition_counts_device(const K* kin, uint64_t n, const K* splitters, int pa
         return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    rc = launch_histogram<K>(kin, n, st, reinterpret_cast<uint32_t*>(t + L.lookback), L.tiles, dz, kPlanKeepTrivial,
+    rc = launch_histogram<K>(kin, n, st, reinterpret_cast<LbWord*>(t + L.lookback), L.tiles, dz, kPlanKeepTrivial,
                              true, s);
     if (rc) return rc;
     k_copy_part_counts<<<1, kMaxParts, 0, s>>>(st, counts, parts);
@@ -857,8 +917,8 @@ int partition_counts_device(const K* kin, uint64_t n, const K* splitters, int pa
 
 template <typename K>
 int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, const K* splitters, int parts, int vmode,
-                             void* const* key_dst, void* const* val_dst, void* temp, size_t temp_bytes,
-                             cudaStream_t s) {
+                             void* const* key_dst, void* const* val_dst, const unsigned long long* dst_table,
+                             void* temp, size_t temp_bytes, cudaStream_t s) {
     DestDigitizer<K> dz;
     int rc = make_dest_digitizer(splitters, parts, &dz);
     if (rc) return rc;
@@ -866,13 +926,15 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
         return set_error(ISORT_EINVAL, "isort_partition: bad vals_mode %d", vmode);
     if (n == 0) return ISORT_OK;
     const bool vals = vmode != ISORT_VALS_NONE;
-    if (!kin || !key_dst || (vals && !val_dst) || (vmode == ISORT_VALS_LOAD && !vin))
+    if (!kin || (!dst_table && (!key_dst || (vals && !val_dst))) || (vmode == ISORT_VALS_LOAD && !vin))
         return set_error(ISORT_EINVAL, "isort_partition: null buffer");
     const RadixLayout L = radix_layout<K>(n, true);
     if (!temp || temp_bytes < L.total)
         return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     ScatterTable tbl{};
-    for (int p = 0; p < parts; ++p) {
+    tbl.dev = dst_table;
+    tbl.parts = parts;
+    for (int p = 0; p < parts && !dst_table; ++p) {
         tbl.key[p] = reinterpret_cast<unsigned long long>(key_dst[p]);
         tbl.val[p] = vals ? reinterpret_cast<unsigned long long>(val_dst[p]) : 0ull;
     }
@@ -880,9 +942,9 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
     const ScatterTable& scat = tbl;  // a kernel argument (by value): no copy, no host sync
     // the look-back words and the ticket of the (single) pass slot start from zero
-    ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * sizeof(uint32_t), s));
+    ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * sizeof(LbWord), s));
     ISORT_CUDA_TRY(cudaMemsetAsync(&st->tile_ticket[0], 0, sizeof(st->tile_ticket), s));
-    auto* lb = reinterpret_cast<uint32_t*>(t + L.lookback);
+    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
     const bool iota = vmode == ISORT_VALS_IOTA;
     // the layout is the payload one (it covers both); the tile count must match the
     // pass configuration actually launched (keys-only tiles are twice as long)
@@ -923,6 +985,25 @@ int isort_rank_mode(void) {
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return -1;
     return rank_fast_path_ok() ? 1 : 0;
+}
+
+int isort_pool_trim(int device) {
+    cudaStream_t s;
+    int rc = use_device(device, &s);
+    if (rc) return rc;
+    cudaMemPool_t pool;
+    if ((rc = lib_pool(&pool))) return rc;
+    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    ISORT_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+    return ISORT_OK;
+}
+
+int isort_init(int device) {
+    cudaStream_t s;
+    int rc = use_device(device, &s);
+    if (rc) return rc;
+    if (rank_state() < 0) return set_error(ISORT_ECUDA, "isort_init: the lane-order self-test could not run");
+    return ISORT_OK;
 }
 
 int isort_profile_begin(void) {
@@ -1248,7 +1329,16 @@ int isort_partition_scatter_u32(const uint32_t* keys_in, const uint32_t* vals_in
                                 const uint32_t* splitters, int parts, int vals_mode, void* const* key_dst,
                                 void* const* val_dst, void* temp, size_t temp_bytes, void* stream) {
     return partition_scatter_device<uint32_t>(keys_in, vals_in, n, splitters, parts, vals_mode, key_dst, val_dst,
-                                              temp, temp_bytes, static_cast<cudaStream_t>(stream));
+                                              nullptr, temp, temp_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int isort_partition_scatter_table_u32(const uint32_t* keys_in, const uint32_t* vals_in, uint64_t n,
+                                      const uint32_t* splitters, int parts, int vals_mode,
+                                      const uint64_t* dst_table, void* temp, size_t temp_bytes, void* stream) {
+    if (!dst_table) return set_error(ISORT_EINVAL, "isort_partition: null destination table");
+    return partition_scatter_device<uint32_t>(keys_in, vals_in, n, splitters, parts, vals_mode, nullptr, nullptr,
+                                              reinterpret_cast<const unsigned long long*>(dst_table), temp,
+                                              temp_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int isort_ipc_alloc(size_t bytes, int device, void** ptr, unsigned char* handle) {

@@ -11,7 +11,10 @@ namespace isort {
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;  // bins per digit pass
 constexpr int kMaxDigits = 8;            // u64 keys: 8 x 8-bit digits
-constexpr int kNumSMs = 148;             // B200; grids are sized in multiples of this
+
+// Number of SMs of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device; 148 on B200).  Persistent grids are sized in multiples of it.
+int sm_count();
 
 template <typename K>
 struct KeyTraits;
@@ -35,6 +38,14 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
 
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Streaming read-only load (input keys are read exactly once per pass).

@@ -28,7 +28,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // Grid for a grid-stride kernel over n items: enough CTAs, at most per_sm per SM.
 inline unsigned grid_for(uint64_t n, int block = 256, int per_sm = 8) {
     const uint64_t want = (n + block - 1) / block;
-    const uint64_t cap = static_cast<uint64_t>(per_sm) * kNumSMs;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * sm_count();
     return static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
 }
 

@@ -29,12 +29,15 @@ namespace isort {
 // Buffer ids used by the plan.
 enum : int32_t { kBufIn = 0, kBufOut = 1, kBufAlt = 2 };
 
-// Look-back status word: [31:30] flag, [29:0] count.
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 2u << 30;
-constexpr uint32_t kFlagMask = 3u << 30;
-constexpr uint32_t kValueMask = (1u << 30) - 1;
-constexpr uint64_t kMaxLookbackN = (1ull << 30) - 1;
+// Look-back status word: [63:62] flag, [61:0] count.  64-bit, so a per-digit
+// prefix never overflows: one call sorts up to 2^32 - 1 keys (positions and
+// payloads are u32; 16 GB of u32 keys per array fits the B200's HBM).
+using LbWord = unsigned long long;
+constexpr LbWord kFlagAgg = 1ull << 62;
+constexpr LbWord kFlagInc = 2ull << 62;
+constexpr LbWord kFlagMask = 3ull << 62;
+constexpr LbWord kValueMask = kFlagAgg - 1;
+constexpr uint64_t kMaxLookbackN = 0xFFFFFFFFull;
 
 struct RadixState {
     uint32_t hist[kMaxDigits][kRadix];  // K1
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     unsigned long long first_bad = ~0ull;
 
     // The range check only exists where keys can exceed M: a template split keeps
-    // its compares out of the common loop.  Indices are 32-bit (n < 2^30).
+    // its compares out of the common loop.  Indices are 32-bit (n < 2^32).
     auto run = [&](auto check_tag) {
         constexpr bool CHECK = decltype(check_tag)::value;
         auto visit = [&](K k, uint32_t idx) {
@@ -319,6 +322,11 @@ constexpr int kScatterMax = 64;
 struct ScatterTable {
     unsigned long long key[kScatterMax];
     unsigned long long val[kScatterMax];
+    // Device-resident alternative: dev[d] = key base of digit d, dev[parts + d] = payload
+    // base (a table computed on the device from the gathered count matrix, so the host
+    // never has to read the matrix before the launch).  Used when non-null.
+    const unsigned long long* dev;
+    int parts;
 };
 // Kernel argument: the table by value for a scatter pass (1 KB of parameters, no
 // copy or synchronisation on the host), nothing otherwise.
@@ -341,11 +349,11 @@ constexpr int kHotDigits = 32;  // <= this many distinct digits in a tile: warp-
 
 // Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back,
 // all kLookbackWindow loads in flight per round trip.
-__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ lb, int t_start, int d,
+__device__ __forceinline__ uint32_t lookback_digit(const LbWord* __restrict__ lb, int t_start, int d,
                                                    uint32_t excl) {
     int t = t_start;
     while (t >= 0) {
-        uint32_t sv[kLookbackWindow];
+        LbWord sv[kLookbackWindow];
 #pragma unroll
         for (int j = 0; j < kLookbackWindow; ++j)
             sv[j] = (t - j >= 0) ? ld_relaxed_gpu(&lb[static_cast<size_t>(t - j) * kRadix + d]) : kFlagInc;
@@ -354,9 +362,9 @@ __device__ __forceinline__ uint32_t lookback_digit(const uint32_t* __restrict__ 
 #pragma unroll
         for (int j = 0; j < kLookbackWindow; ++j) {
             if (!done && used == j) {
-                const uint32_t f = sv[j] & kFlagMask;
+                const LbWord f = sv[j] & kFlagMask;
                 if (f != 0) {
-                    excl += sv[j] & kValueMask;
+                    excl += static_cast<uint32_t>(sv[j] & kValueMask);
                     used = j + 1;
                     done = (f == kFlagInc);
                 }
@@ -611,7 +619,7 @@ template <typename K, typename Dz, int BLOCK, int IPT, int NCHUNK, bool VALS, bo
 __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     k_onesweep(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
-               int iota_vals, uint64_t n, RadixState* __restrict__ st, uint32_t* __restrict__ lookback,
+               int iota_vals, uint64_t n, RadixState* __restrict__ st, LbWord* __restrict__ lookback,
                uint32_t num_tiles, int slot, Dz dz, const ScatterArg<SCATTER> scat) {
     using Smem = OnesweepSmem<K, BLOCK, IPT, NCHUNK, VALS, !Dz::kCheapDigit>;
     constexpr bool kBulkWrite = ISORT_PASS_BULK && !SCATTER;  // peer stores (SCATTER) stay per key
@@ -633,7 +641,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     uint32_t* vdst = dst_id == kBufOut ? vals_out : vals_alt;
     const bool gen_iota = iota_vals && slot == 0;
     const uint32_t dsh = dz.shift_for(pos);
-    uint32_t* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
+    LbWord* lb = lookback + static_cast<size_t>(slot) * num_tiles * kRadix;
     const bool vec = sizeof(K) == 4 && IPT % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
 #ifndef ISORT_POL_KEEP
 #define ISORT_POL_KEEP policy_evict_last()
@@ -652,9 +660,16 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
     if constexpr (SCATTER) {
         if (tid < kScatterMax) {  // per-digit base, shifted so that base + g addresses the run
             const unsigned long long o = st->offs[pos][tid];
-            s_kbase[tid] = scat.key[tid] - o * sizeof(K);
-            if (VALS) s_vbase[tid] = scat.val[tid] - o * sizeof(uint32_t);
+            const bool dev = scat.dev != nullptr;
+            const unsigned long long kb = dev ? (tid < scat.parts ? scat.dev[tid] : 0ull) : scat.key[tid];
+            s_kbase[tid] = kb - o * sizeof(K);
+            if (VALS) {
+                const unsigned long long vb = dev ? (tid < scat.parts ? scat.dev[scat.parts + tid] : 0ull) : scat.val[tid];
+                s_vbase[tid] = vb - o * sizeof(uint32_t);
+            }
         }
+        // a zeroed device table means "does not fit" (the caller falls back): store nothing
+        if (__syncthreads_or(scat.dev != nullptr && tid < scat.parts && scat.dev[tid] == 0ull)) return;
     }
 
 #ifdef ISORT_PHASE_TIMING
@@ -705,7 +720,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
             nonzero = tot != 0;
             uint32_t excl = 0;
             if (tile == 0) {
-                st_relaxed_gpu(&lb[d], kFlagInc | tot);
+                st_relaxed_gpu(&lb[d], kFlagInc | tot);  // (tot, excl: u32 counts, zero-extended)
             } else {
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], kFlagAgg | tot);
 #ifndef ISORT_AB_NO_LOOKBACK

@@ -39,22 +39,24 @@ def _stream(seed: int, start: int, count: int, step: int = 1, offset: int = 1) -
         return mix64(np.uint64(seed) + (j + np.uint64(offset)) * GAMMA)
 
 
-def uniform_u32(n: int, seed: int = 42, bits: int = 32, chunk: int = 1 << 24) -> np.ndarray:
-    """Keys of generate({case 1, n, M = 2^bits - 1, seed}) as uint32."""
+def uniform_u32(n: int, seed: int = 42, bits: int = 32, chunk: int = 1 << 24, start: int = 0) -> np.ndarray:
+    """Keys start .. start+n-1 of generate({case 1, M = 2^bits - 1, seed}) as uint32
+    (the stream is counter-based: a shard is generated without the keys before it)."""
     out = np.empty(n, dtype=np.uint32)
     mask = np.uint64((1 << bits) - 1)
     for s in range(0, n, chunk):
         c = min(chunk, n - s)
         with np.errstate(over="ignore"):
-            out[s:s + c] = (_stream(seed, s, c) & mask).astype(np.uint32)
+            out[s:s + c] = (_stream(seed, start + s, c) & mask).astype(np.uint32)
     return out
 
 
-def mixture_u32(n: int, seed: int = 42, chunk: int = 1 << 22) -> np.ndarray:
+def mixture_u32(n: int, seed: int = 42, chunk: int = 1 << 22, start: int = 0) -> np.ndarray:
+    """Keys start .. start+n-1 of the config-5 mixture (counter-based, like uniform_u32)."""
     out = np.empty(n, dtype=np.uint32)
     for s in range(0, n, chunk):
         c = min(chunk, n - s)
-        i = np.arange(s, s + c, dtype=np.uint64)
+        i = np.arange(start + s, start + s + c, dtype=np.uint64)
         with np.errstate(over="ignore"):
             x0 = mix64(np.uint64(seed) + (np.uint64(3) * i + np.uint64(1)) * GAMMA)
             x1 = mix64(np.uint64(seed) + (np.uint64(3) * i + np.uint64(2)) * GAMMA)
@@ -71,6 +73,8 @@ def mixture_u32(n: int, seed: int = 42, chunk: int = 1 << 22) -> np.ndarray:
 def config_keys(name: str, n: int | None = None, seed: int = 42) -> np.ndarray:
     """Keys (uint32) of a BASELINE configuration by name: c1, c2, c3, c4a, c4b, c5."""
     name = name.lower()
+    if name == "c5" and (n or 10**9) >= (1 << 24):
+        return mixture_u32_parallel(n or 10**9, seed)
     if name in ("c1", "c2"):
         return uniform_u32(n or (10**6 if name == "c1" else 10**8), seed)
     if name == "c3":
@@ -81,6 +85,39 @@ def config_keys(name: str, n: int | None = None, seed: int = 42) -> np.ndarray:
     if name == "c5":
         return mixture_u32(n or 10**9, seed)
     raise KeyError(name)
+
+
+def mixture_u32_parallel(n: int, seed: int = 42, start: int = 0, threads: int | None = None) -> np.ndarray:
+    """mixture_u32 over host threads (numpy drops the GIL in its kernels): the same
+    values, each thread filling its own index range."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = np.empty(n, dtype=np.uint32)
+    threads = threads or min(32, os.cpu_count() or 1)
+    step = max(1 << 22, (n + threads - 1) // threads)
+
+    def part(s):
+        c = min(step, n - s)
+        out[s:s + c] = mixture_u32(c, seed, start=start + s)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(part, range(0, n, step)))
+    return out
+
+
+def config_shard(name: str, n_total: int, rank: int, world: int, seed: int = 42) -> np.ndarray:
+    """Rank `rank`'s positional shard [r*n/G, (r+1)*n/G) of a configuration's
+    n_total keys: the G shards concatenated are exactly config_keys(name, n_total)."""
+    lo, hi = n_total * rank // world, n_total * (rank + 1) // world
+    name = name.lower()
+    if name in ("c1", "c2"):
+        return uniform_u32(hi - lo, seed, start=lo)
+    if name == "c3":
+        return uniform_u32(hi - lo, seed, bits=10, start=lo)
+    if name == "c5":
+        return mixture_u32_parallel(hi - lo, seed, start=lo)
+    return config_keys(name, n_total, seed)[lo:hi].copy()
 
 
 def config_range_bound(name: str) -> int:

@@ -59,6 +59,18 @@ class PhaseTimes:
     local_sort: float = 0.0
     received: int = 0
     extra: dict = field(default_factory=dict)
+    events: tuple = ()
+
+    def resolve(self, ops) -> "PhaseTimes":
+        """Turn the recorded events into per-phase times (waits for the last one)."""
+        if self.events:
+            e0, e1, e2, e3, e4 = self.events
+            self.splitters = ops.elapsed(e0, e1)
+            self.partition = ops.elapsed(e1, e2)
+            self.exchange = ops.elapsed(e2, e3)
+            self.local_sort = ops.elapsed(e3, e4)
+            self.events = ()
+        return self
 
 
 class CudaOps:
@@ -69,11 +81,13 @@ class CudaOps:
         self.lib = _lib.load()
 
     def sample(self, keys: torch.Tensor, s: int) -> torch.Tensor:
+        """Exactly s keys: evenly spaced positions (cyclic when n < s); an empty
+        shard contributes the largest key value (it only shifts quantiles)."""
         n = keys.numel()
         if n == 0:
-            return keys[:0].clone()
-        step = max(1, n // s)
-        return keys[::step][:s].contiguous()
+            return torch.full((s,), -1, dtype=keys.dtype, device=keys.device)
+        pos = (torch.arange(s, device=keys.device, dtype=torch.int64) * n) // s
+        return keys[pos].contiguous()
 
     def sort(self, keys: torch.Tensor) -> torch.Tensor:
         from .device import radix_sort
@@ -117,6 +131,20 @@ class CudaOps:
         _lib.check(self.lib.isort_partition_counts_u32(keys.data_ptr(), n, spl, parts, counts.data_ptr(),
                                                        temp.data_ptr(), tb, s))
         return counts
+
+    def partition_scatter_table(self, keys, vals, splitters: list[int], parts: int, table: torch.Tensor):
+        """Fused path, step 2 with the destination table on the device (int64,
+        [key bases..., payload bases...]): no host read of the count matrix."""
+        import ctypes
+
+        n = keys.numel()
+        temp, tb = self._temp(n)
+        spl = (ctypes.c_uint32 * max(1, parts - 1))(*[int(x) & 0xFFFFFFFF for x in splitters])
+        vmode = _lib.VALS_LOAD if vals is not None else _lib.VALS_NONE
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.isort_partition_scatter_table_u32(
+            keys.data_ptr(), vals.data_ptr() if vals is not None else None, n, spl, parts, vmode, table.data_ptr(),
+            temp.data_ptr(), tb, s))
 
     def partition_scatter(self, keys, vals, splitters: list[int], parts: int, key_dst: list[int],
                           val_dst: list[int] | None):
@@ -247,6 +275,8 @@ class PeerBuffers:
         except Exception:  # noqa: BLE001
             ok.zero_()
         self._agree(ok, "open")
+        self.key_table = torch.tensor(self.key_bases, dtype=torch.int64, device=device)
+        self.val_table = torch.tensor(self.val_bases, dtype=torch.int64, device=device)
 
     def _agree(self, ok: torch.Tensor, what: str) -> None:
         self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
@@ -281,28 +311,25 @@ class KeyRangeSorter:
         self.last_path = None
 
     def splitters(self, keys: torch.Tensor) -> list[int]:
-        """G-1 ascending splitter key values from the gathered sample's quantiles."""
+        """G-1 ascending splitter key values from the gathered sample's quantiles.
+
+        Every rank contributes exactly `sample_per_rank` keys (a strided sample,
+        repeated cyclically when the shard is smaller; an empty shard sends the
+        largest key), so one all_gather of fixed size suffices and the only host
+        read is the G-1 splitters themselves -- kernel parameters of the
+        partition pass (DestDigitizer): compared in registers against constant-bank
+        operands, cheaper per key than any device-memory lookup."""
         g = self.world
         if g == 1:
             return []
         smp = self.ops.sample(keys, self.sample_per_rank)
-        sizes = torch.tensor([smp.numel()], dtype=torch.int64, device=smp.device)
-        all_sizes = [torch.zeros_like(sizes) for _ in range(g)]
-        self.dist.all_gather(all_sizes, sizes)
-        sz = [int(x.item()) for x in all_sizes]
-        m = max(sz) if sz else 0
-        padded = torch.zeros(m, dtype=smp.dtype, device=smp.device)
-        padded[: smp.numel()] = smp
-        gathered = [torch.zeros_like(padded) for _ in range(g)]
-        self.dist.all_gather(gathered, padded)
-        pool = torch.cat([t[:s] for t, s in zip(gathered, sz)])
-        if pool.numel() == 0:
-            return [self.key_max] * (g - 1)
-        srt = self.ops.sort(pool)
+        gathered = [torch.empty_like(smp) for _ in range(g)]
+        self.dist.all_gather(gathered, smp)
+        srt = self.ops.sort(torch.cat(gathered))
         # quantile i*len/g (as unsigned key values); equal keys never straddle ranks
-        idx = [min(srt.numel() - 1, (i * srt.numel()) // g) for i in range(1, g)]
-        vals = srt[torch.tensor(idx, device=srt.device)]
-        out = [int(v) & 0xFFFFFFFF for v in vals.tolist()]
+        m = srt.numel()
+        idx = torch.tensor([min(m - 1, (i * m) // g) for i in range(1, g)], device=srt.device)
+        out = [int(v) & 0xFFFFFFFF for v in srt[idx].tolist()]
         for i in range(1, len(out)):  # ascending (duplicates allowed: empty ranges)
             out[i] = max(out[i], out[i - 1])
         return out
@@ -310,27 +337,40 @@ class KeyRangeSorter:
     def _fused_exchange(self, keys, vals, spl):
         """Counts -> gathered count matrix -> partition pass storing into the peers'
         receive buffers -> on-stream barrier.  Returns (keys, payload) views of this
-        rank's receive buffer, or None when some rank's share exceeds the capacity."""
+        rank's receive buffer, or None when some rank's share exceeds the capacity.
+
+        The count matrix stays on the device: the destination table (peer base +
+        the runs of lower source ranks, fused_destinations) is computed there and
+        the partition kernel reads it from device memory.  The host reads only this
+        rank's received total and the largest total (the local sort's size and the
+        capacity check), with the copy queued behind the partition kernel so the
+        round trip overlaps it."""
         g, me, pb = self.world, self.rank, self.peers
         counts = self.ops.partition_counts(keys, spl, g)
         allc = [torch.zeros_like(counts) for _ in range(g)]
         self.dist.all_gather(allc, counts)
-        matrix = [[int(x) for x in row.tolist()] for row in allc]
-        totals = recv_totals(matrix)
-        if max(totals) > pb.capacity:
+        matrix = torch.stack(allc)  # row = source rank, column = destination rank (int64, device)
+        totals = matrix.sum(dim=0)
+        before = matrix[:me].sum(dim=0) if me > 0 else torch.zeros_like(totals)  # runs of lower source ranks
+        fits = totals.max() <= pb.capacity
+        table = torch.cat([pb.key_table + 4 * before, pb.val_table + 4 * before])
+        table = torch.where(fits, table, torch.zeros_like(table))  # never store out of bounds
+        self.ops.partition_scatter_table(keys, vals, spl, g, table)
+        info = torch.stack([totals[me], fits.to(totals.dtype)]).cpu()  # after the kernel in stream order
+        if not bool(info[1]):
             return None
-        kd = fused_destinations(matrix, me, pb.key_bases, 4)
-        vd = fused_destinations(matrix, me, pb.val_bases, 4) if vals is not None else None
-        self.ops.partition_scatter(keys, vals, spl, g, kd, vd)
+        total = int(info[0])
         flag = torch.zeros(1, dtype=torch.int32, device=keys.device)
         self.dist.all_reduce(flag)  # every peer's stores precede the local sort
-        out = device_view(pb.key_bases[me], totals[me], keys.device)
-        vout = device_view(pb.val_bases[me], totals[me], keys.device) if vals is not None else None
+        out = device_view(pb.key_bases[me], total, keys.device)
+        vout = device_view(pb.val_bases[me], total, keys.device) if vals is not None else None
         return out, vout
 
     def sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None, algorithm: str = "radix",
-             force_nccl: bool = False):
-        """Returns (this rank's sorted key range, payload or None, PhaseTimes)."""
+             force_nccl: bool = False, resolve: bool = True):
+        """Returns (this rank's sorted key range, payload or None, PhaseTimes).
+        resolve=False leaves the phase events unread (PhaseTimes.resolve later), so
+        back-to-back sorts are not serialised by the timing."""
         g, me = self.world, self.rank
         pt = PhaseTimes()
         e0 = self.ops.event()
@@ -354,8 +394,9 @@ class KeyRangeSorter:
             # count matrix: row = source rank, column = destination rank
             allc = [torch.zeros_like(counts) for _ in range(g)]
             self.dist.all_gather(allc, counts)
-            send = [int(x) for x in counts.tolist()]
-            recv = [int(allc[src][me].item()) for src in range(g)]
+            # all_to_all_single takes its split sizes on the host: one read of both
+            sr = torch.cat([counts, torch.stack(allc)[:, me]]).tolist()
+            send, recv = [int(x) for x in sr[:g]], [int(x) for x in sr[g:]]
             out = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
             _all_to_all(self.dist, out, parted, recv, send)
             vout = None
@@ -370,10 +411,9 @@ class KeyRangeSorter:
         hi = max(hi, lo)
         sk, sv = self.ops.local_sort(out, vout, algorithm, lo, hi)
         e4 = self.ops.event()
-        pt.splitters = self.ops.elapsed(e0, e1)
-        pt.partition = self.ops.elapsed(e1, e2)
-        pt.exchange = self.ops.elapsed(e2, e3)
-        pt.local_sort = self.ops.elapsed(e3, e4)
+        pt.events = (e0, e1, e2, e3, e4)
+        if resolve:
+            pt.resolve(self.ops)
         pt.received = int(out.numel())
         return sk, sv, pt
 
@@ -406,45 +446,54 @@ def enable_fused(sorter: KeyRangeSorter, keys: torch.Tensor, algorithm: str, sla
 def bench_distributed(keys: torch.Tensor, algorithm: str, range_bound: int, steps: int, warmup: int, dist):
     """Time `steps` distributed sorts of the per-rank shards (bench.py, N > 1).
 
-    Device time per step = max over ranks of (CUDA-event time from the first
-    barrier to the end of the local sort).  Returns (ms_per_step, info)."""
+    Device time per step = max over ranks of (CUDA-event time from the barrier
+    to the end of the last local sort) / steps.  Returns (ms_per_step, info,
+    this rank's sorted key range from the last step)."""
     import os
 
     dev = keys.device
-    sorter = KeyRangeSorter(dist, CudaOps(dev))
-    if os.environ.get("ISORT_FUSED_EXCHANGE", "1") != "0":
-        enable_fused(sorter, keys, algorithm)
-    l0 = _lib.load().isort_launch_count()
-    for _ in range(warmup):
-        sorter.sort(keys, algorithm=algorithm)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    torch.cuda.synchronize(dev)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    phases = []
-    l1 = _lib.load().isort_launch_count()
-    start.record()
-    for _ in range(steps):
-        _, _, pt = sorter.sort(keys, algorithm=algorithm)
-        phases.append(pt)
-    end.record()
-    torch.cuda.synchronize(dev)
-    launches = _lib.load().isort_launch_count() - l1
-    ms = torch.tensor([start.elapsed_time(end) / steps], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    avg = {k: sum(getattr(p, k) for p in phases) / len(phases)
-           for k in ("splitters", "partition", "exchange", "local_sort")}
-    recv = torch.tensor([float(phases[-1].received)], device=dev)
-    mx = recv.clone()
-    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    mean = recv.clone()
-    dist.all_reduce(mean, op=dist.ReduceOp.SUM)
-    info = {"phases": {k: round(v, 4) for k, v in avg.items()}, "launches": int(launches),
-            "max_over_mean_received": float(mx.item() / max(1.0, mean.item() / dist.get_world_size())),
-            "warmup_launches": int(l1 - l0),
-            "exchange": "fused (partition stores into peer receive buffers over NVLink)" if sorter.peers is not None
-            else "nccl all_to_all"}
-    return float(ms.item()), info
+    ops = CudaOps(dev)
+    sorter = KeyRangeSorter(dist, ops)
+    try:
+        if os.environ.get("ISORT_FUSED_EXCHANGE", "1") != "0":
+            enable_fused(sorter, keys, algorithm)
+        l0 = _lib.load().isort_launch_count()
+        for _ in range(warmup):
+            sorter.sort(keys, algorithm=algorithm)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        phases = []
+        l1 = _lib.load().isort_launch_count()
+        start.record()
+        for _ in range(steps):
+            sk, _, pt = sorter.sort(keys, algorithm=algorithm, resolve=False)
+            phases.append(pt)
+        end.record()
+        torch.cuda.synchronize(dev)
+        launches = _lib.load().isort_launch_count() - l1
+        for p in phases:
+            p.resolve(ops)
+        ms = torch.tensor([start.elapsed_time(end) / steps], device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        avg = {k: sum(getattr(p, k) for p in phases) / len(phases)
+               for k in ("splitters", "partition", "exchange", "local_sort")}
+        recv = torch.tensor([float(phases[-1].received)], device=dev)
+        mx = recv.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        mean = recv.clone()
+        dist.all_reduce(mean, op=dist.ReduceOp.SUM)
+        info = {"phases_ms": {k: round(v, 4) for k, v in avg.items()}, "launches": int(launches),
+                "max_over_mean_received": float(mx.item() / max(1.0, mean.item() / dist.get_world_size())),
+                "warmup_launches": int(l1 - l0),
+                "exchange": "fused (partition stores into peer receive buffers over NVLink)"
+                if sorter.peers is not None else "nccl all_to_all"}
+        return float(ms.item()), info, sk.clone()
+    finally:
+        if sorter.peers is not None:
+            sorter.peers.close()
+            sorter.peers = None
 
 
 def _wallclock() -> float:  # pragma: no cover - helper for ad-hoc use

@@ -50,7 +50,7 @@ def test_library_is_sm100a_native():
 def test_abi_version_and_limits():
     lib = _lib.load()
     assert lib.isort_abi_version() == 1
-    assert lib.isort_max_keys() == (1 << 30) - 1
+    assert lib.isort_max_keys() == (1 << 32) - 1
 
 
 def test_reference_argument_errors_without_device():
@@ -90,7 +90,7 @@ def test_device_entry_points_validate_arguments():
     assert rc == _lib.ISORT_EINVAL
     rc = lib.isort_radix_sort_u32(ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, 10, 0, None, 0, None)
     assert rc == _lib.ISORT_EINVAL and b"temp buffer too small" in lib.isort_last_error()
-    rc = lib.isort_radix_sort_u32(ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, 1 << 30, 0, None, 0, None)
+    rc = lib.isort_radix_sort_u32(ctypes.c_void_p(16), ctypes.c_void_p(16), None, None, 1 << 32, 0, None, 0, None)
     assert rc == _lib.ISORT_ERANGE
     assert lib.isort_radix_temp_bytes(10**8, 4, 0) > 4 * 10**8
     assert lib.isort_bucket_temp_bytes(10**8, 4, 2) > lib.isort_radix_temp_bytes(10**8, 4, 2)

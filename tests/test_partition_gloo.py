@@ -25,9 +25,11 @@ def _u(t: torch.Tensor) -> torch.Tensor:
 class TorchCpuOps:
     """Stand-in for CudaOps on CPU tensors (test double, not a product path)."""
 
-    def sample(self, keys, s):
-        step = max(1, keys.numel() // s)
-        return keys[::step][:s].contiguous()
+    def sample(self, keys, s):  # CudaOps.sample's contract: exactly s keys
+        n = keys.numel()
+        if n == 0:
+            return torch.full((s,), -1, dtype=keys.dtype)
+        return keys[(torch.arange(s, dtype=torch.int64) * n) // s].contiguous()
 
     def sort(self, keys):
         return keys[torch.sort(_u(keys), stable=True).indices]
