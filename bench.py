@@ -466,6 +466,9 @@ def gather_to_rank0(dist, t, dev):
     import torch
 
     world, rank = dist.get_world_size(), dist.get_rank()
+    if dist.get_backend() == "gloo":  # gloo's point-to-point moves host memory only
+        dev = torch.device("cpu")
+        t = t.cpu()
     size = torch.tensor([t.numel()], dtype=torch.int64, device=dev)
     sizes = [torch.zeros_like(size) for _ in range(world)]
     dist.all_gather(sizes, size)

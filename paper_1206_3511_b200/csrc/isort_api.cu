@@ -208,6 +208,9 @@ namespace isort {
 
 constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
+// Bytes per look-back status word for a call over n keys (radix_onesweep.cuh).
+inline size_t lb_word_bytes(uint64_t n) { return n <= kNarrowLbMaxN ? 4 : 8; }
+
 struct RadixLayout {
     size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
     uint32_t tiles = 0;
@@ -228,7 +231,7 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
     L.state = off;
     off += align_up(sizeof(RadixState));
     L.lookback = off;
-    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * sizeof(LbWord));
+    off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * lb_word_bytes(n));
     L.keys_alt = off;
     off += align_up(n * sizeof(K));
     L.vals_alt = off;
@@ -273,12 +276,18 @@ int resident_per_sm(F* kernel, int block, size_t smem) {
 
 template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false>
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
-                   uint64_t n, RadixState* st, LbWord* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
+                   uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
                    const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{}) {
     constexpr int D = Dz::kDigits;
     using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
-    auto* kern = rank_fast_path_ok() ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER>
-                                     : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER>;
+    using Narrow = uint32_t;            // look-back status words: n < 2^30
+    using Wide = unsigned long long;    // n up to 2^32 - 1
+    const bool fast = rank_fast_path_ok();
+    const bool narrow = lb_word_bytes(n) == 4;
+    auto* kern = fast ? (narrow ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER, Narrow>
+                                : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER, Wide>)
+                      : (narrow ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER, Narrow>
+                                : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER, Wide>);
     set_max_smem_once(kern, sizeof(Smem));
     const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * sm_count()) ? tiles
                                                                                      : Cfg::kCtasPerSm * sm_count();
@@ -294,14 +303,14 @@ void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t
 // Histogram step of a pipeline: zero the state, K1 (all digit histograms, max,
 // sortedness, range check), K2 (scans + pass plan).
 template <typename K, typename Dz>
-int launch_histogram(const K* kin, uint64_t n, RadixState* st, LbWord* lookback, uint32_t tiles, const Dz& dz,
+int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz,
                      int plan_flags, bool zero_state, cudaStream_t s) {
     constexpr int D = Dz::kDigits;
     prof_mark(s, "start");
     g_prof.st = st;
     if (zero_state) {
         const size_t bytes = reinterpret_cast<char*>(lookback) - reinterpret_cast<char*>(st) +
-                             static_cast<size_t>(D) * tiles * kRadix * sizeof(LbWord);
+                             static_cast<size_t>(D) * tiles * kRadix * lb_word_bytes(n);
         ISORT_CUDA_TRY(cudaMemsetAsync(st, 0, bytes, s));
         prof_mark(s, "memset");
     }
@@ -326,7 +335,7 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, LbWord* lookback,
 // as ping-pong; the plan decides which passes run.
 template <typename K, bool VALS, typename Dz>
 int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
-                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, LbWord* lookback,
+                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, void* lookback,
                           uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
                           cudaStream_t s) {
     constexpr int D = Dz::kDigits;
@@ -365,7 +374,7 @@ int radix_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout
         return set_error(ISORT_EINVAL, "isort_radix_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
+    auto* lb = (t + L.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
     RadixDigitizer<K> dz;
@@ -652,7 +661,7 @@ int bucket_finish_impl(const K* kin, K* kout, uint32_t* vout, uint64_t n, uint64
         return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
-    auto* lb = reinterpret_cast<LbWord*>(t + L.r.lookback);
+    auto* lb = (t + L.r.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     if (hs->first_bad_not != 0) {
@@ -745,7 +754,7 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
         return set_error(ISORT_EINVAL, "isort_bucket_sort: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.r.state);
-    auto* lb = reinterpret_cast<LbWord*>(t + L.r.lookback);
+    auto* lb = (t + L.r.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.r.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.r.vals_alt) : nullptr;
     auto* bst = reinterpret_cast<BucketState*>(t + L.bstate);
@@ -856,7 +865,7 @@ int partition_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
         return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
+    auto* lb = (t + L.lookback);
     auto* kalt = reinterpret_cast<K*>(t + L.keys_alt);
     auto* valt = vals ? reinterpret_cast<uint32_t*>(t + L.vals_alt) : nullptr;
     int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, vmode == ISORT_VALS_IOTA, n, st,
@@ -906,7 +915,7 @@ int partition_counts_device(const K* kin, uint64_t n, const K* splitters, int pa
         return set_error(ISORT_EINVAL, "isort_partition: temp buffer too small (%zu < %zu)", temp_bytes, L.total);
     char* t = static_cast<char*>(temp);
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
-    rc = launch_histogram<K>(kin, n, st, reinterpret_cast<LbWord*>(t + L.lookback), L.tiles, dz, kPlanKeepTrivial,
+    rc = launch_histogram<K>(kin, n, st, (t + L.lookback), L.tiles, dz, kPlanKeepTrivial,
                              true, s);
     if (rc) return rc;
     k_copy_part_counts<<<1, kMaxParts, 0, s>>>(st, counts, parts);
@@ -942,9 +951,9 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
     auto* st = reinterpret_cast<RadixState*>(t + L.state);
     const ScatterTable& scat = tbl;  // a kernel argument (by value): no copy, no host sync
     // the look-back words and the ticket of the (single) pass slot start from zero
-    ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * sizeof(LbWord), s));
+    ISORT_CUDA_TRY(cudaMemsetAsync(t + L.lookback, 0, static_cast<size_t>(L.tiles) * kRadix * lb_word_bytes(n), s));
     ISORT_CUDA_TRY(cudaMemsetAsync(&st->tile_ticket[0], 0, sizeof(st->tile_ticket), s));
-    auto* lb = reinterpret_cast<LbWord*>(t + L.lookback);
+    auto* lb = (t + L.lookback);
     const bool iota = vmode == ISORT_VALS_IOTA;
     // the layout is the payload one (it covers both); the tile count must match the
     // pass configuration actually launched (keys-only tiles are twice as long)

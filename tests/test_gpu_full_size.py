@@ -75,3 +75,24 @@ def test_full_size_bit_exact(cuda, oracle, checks, cfg):
         ko, _ = sort_on_device(keys, alg, None, bound)
         assert sha(ko) == c["sorted_keys_sha256"], f"{cfg} {alg} (keys only): sorted keys differ"
         del ko
+
+
+def test_beyond_2_pow_30_keys_per_call(cuda):
+    """n > 2^30: the passes switch to 64-bit look-back status words (a 32-bit
+    word's 30-bit count would overflow).  A stable sort is unique, so checking
+    (a) keys sorted, (b) keys_out == keys_in[positions] (a permutation that carries
+    each key) and (c) positions ascending inside every run of equal keys (there are
+    ~10^8 such pairs among 2^30 random u32 keys) proves bit-exactness at this size."""
+    from paper_1206_3511_b200 import _lib, inputs
+
+    n = (1 << 30) + 12_345
+    assert n > 2**30 and n <= _lib.load().isort_max_keys()
+    keys = inputs.uniform_u32(n, seed=2026)
+    for alg in ("radix", "bucket"):
+        ko, vo = sort_on_device(keys, alg, "iota", (1 << 32) - 1)
+        assert bool(np.all(ko[1:] >= ko[:-1])), alg
+        assert np.array_equal(keys[vo], ko), alg
+        eq = ko[1:] == ko[:-1]
+        assert int(eq.sum()) > 10**7
+        assert bool(np.all(vo[1:][eq] > vo[:-1][eq])), f"{alg}: unstable"
+        del ko, vo, eq
