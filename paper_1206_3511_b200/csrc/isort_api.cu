@@ -350,9 +350,23 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
                                                         dz, s);
     launched(D);
     const uint64_t cblocks = (n + 4095) / 4096;
-    k_copy_if_unsorted_skip<K><<<static_cast<unsigned>(cblocks < 4ull * sm_count() ? (cblocks ? cblocks : 1) : 4ull * sm_count()), 512, 0, s>>>(
-        kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
+    const unsigned cgrid = static_cast<unsigned>(cblocks < 4ull * sm_count() ? (cblocks ? cblocks : 1) : 4ull * sm_count());
+    k_copy_if_unsorted_skip<K><<<cgrid, 512, 0, s>>>(kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
     prof_mark(s, "copy");
+    // non-increasing input (the plan's reverse early-out): the run-wise reversal
+    if (!VALS) {
+        k_reverse_keys<K><<<cgrid, 512, 0, s>>>(kin, kout, n, st);
+        launched(2);
+    } else {
+        auto* head = static_cast<long long*>(lookback);  // the look-back rows are unused on this path
+        auto* end = head + (n + kRevTile - 1) / kRevTile;
+        const unsigned rgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
+        k_rev_tile_bounds<K><<<rgrid, kRevBlock, 0, s>>>(kin, n, st, head, end);
+        k_rev_carry<<<1, 1024, 0, s>>>(n, st, head, end);
+        k_rev_scatter<K, true><<<rgrid, kRevBlock, 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st, head, end);
+        launched(4);
+    }
+    prof_mark(s, "reverse");
     ISORT_CUDA_TRY(cudaGetLastError());
     return ISORT_OK;
 }

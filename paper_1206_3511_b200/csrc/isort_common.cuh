@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 #define ISORT_FULL_MASK 0xffffffffu
 
@@ -98,6 +99,21 @@ __device__ __forceinline__ T warp_max(T v) {
         v = t > v ? t : v;
     }
     return v;
+}
+
+// Block-wide max of a 64-bit value (BLOCK threads, all participating); the
+// result is valid in every thread.  Two barriers.
+template <int BLOCK>
+__device__ __forceinline__ long long block_reduce_max_ll(long long v) {
+    __shared__ long long s_red[BLOCK / 32];
+    v = warp_max<long long>(v);
+    __syncthreads();
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    long long r = s_red[0];
+#pragma unroll
+    for (int w = 1; w < BLOCK / 32; ++w) r = r > s_red[w] ? r : s_red[w];
+    return r;
 }
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {

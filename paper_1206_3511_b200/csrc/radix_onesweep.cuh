@@ -51,8 +51,10 @@ struct RadixState {
     unsigned long long max_key;         // K1
     unsigned long long first_bad;       // K1: ~(first index failing the range check)
     uint32_t descents;                  // K1: #i with key[i] > key[i+1]
+    uint32_t ascents;                   // K1: #i with key[i] < key[i+1] (0 => non-increasing)
     uint32_t n_active;                  // K2
-    uint32_t copy_in_to_out;            // K2
+    uint32_t copy_in_to_out;            // K2: sorted input, out = in
+    uint32_t reversed;                  // K2: non-increasing input, out = in reversed run by run
     uint32_t tile_ticket[kMaxDigits];   // K3
     int32_t digit_of_slot[kMaxDigits];  // K2
     int32_t src_of_slot[kMaxDigits];
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     uint32_t* const my_cnt = uf_cnt + lane_id() % R;  // this lane's counter copy
 
     K kmax = 0;
-    uint32_t desc = 0;
+    uint32_t desc = 0, asc = 0;
     unsigned long long first_bad = ~0ull;
 
     // The range check only exists where keys can exceed M: a template split keeps
@@ -170,6 +172,8 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
                     if (v + 1 == nv) next = tail_next;
                     if (v < nv) {
                         desc += (k[u][0] > k[u][1]) + (k[u][1] > k[u][2]) + (k[u][2] > k[u][3]) + (k[u][3] > next);
+                        asc |= (k[u][0] < k[u][1]) | (k[u][1] < k[u][2]) | (k[u][2] < k[u][3]) |
+                               (k[u][3] < next && v + 1 < nv) | (k[u][3] < next && v + 1 == nv && nv * V < n32);
 #pragma unroll
                         for (int j = 0; j < V; ++j) visit(k[u][j], v * V + j);
                     }
@@ -177,13 +181,19 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
             }
             for (uint32_t i = nv * V + blockIdx.x * BLOCK + threadIdx.x; i < n32; i += stride) {
                 const K k = keys[i];
-                if (i + 1 < n32) desc += (k > keys[i + 1]);
+                if (i + 1 < n32) {
+                    desc += (k > keys[i + 1]);
+                    asc |= (k < keys[i + 1]);
+                }
                 visit(k, i);
             }
         } else {
             for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n32; i += stride) {
                 const K k = keys[i];
-                if (i + 1 < n32) desc += (k > keys[i + 1]);
+                if (i + 1 < n32) {
+                    desc += (k > keys[i + 1]);
+                    asc |= (k < keys[i + 1]);
+                }
                 visit(k, i);
             }
         }
@@ -196,6 +206,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
     // block reductions
     unsigned long long m = warp_max<unsigned long long>(static_cast<unsigned long long>(kmax));
     uint32_t ds = warp_sum(desc);
+    if (__any_sync(ISORT_FULL_MASK, asc != 0) && lane_id() == 0) atomicOr(&st->ascents, 1u);
     unsigned long long fb = warp_max<unsigned long long>(~first_bad);  // max of complements = min index
     const int w = threadIdx.x / 32;
     if (lane_id() == 0) {
@@ -246,16 +257,20 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
     }
     if (t == 0) {
         const bool sorted = (flags & kPlanSkipSorted) && st->descents == 0;
+        // non-increasing input: the stable sort is the reversal with each run of
+        // equal keys kept in input order (k_reverse_runs), no digit pass
+        const bool reversed = (flags & kPlanSkipSorted) && !sorted && st->ascents == 0;
         const bool keep = (flags & kPlanKeepTrivial) != 0;
         int na = 0;
         for (int p = 0; p < D; ++p)
-            if (keep || (!sorted && !trivial[p])) st->digit_of_slot[na++] = p;
+            if (keep || (!sorted && !reversed && !trivial[p])) st->digit_of_slot[na++] = p;
         for (int s = 0; s < na; ++s) {
             st->src_of_slot[s] = s == 0 ? kBufIn : st->dst_of_slot[s - 1];
             st->dst_of_slot[s] = ((na - 1 - s) % 2 == 0) ? kBufOut : kBufAlt;
         }
         st->n_active = na;
-        st->copy_in_to_out = na == 0;
+        st->copy_in_to_out = na == 0 && !reversed;
+        st->reversed = reversed;
     }
 }
 
@@ -882,6 +897,158 @@ __global__ void k_copy_if_unsorted_skip(const K* __restrict__ in, K* __restrict_
     for (uint64_t i = done + t0; i < n; i += stride) out[i] = in[i];
     if (vout) {
         for (uint64_t i = t0; i < n; i += stride) vout[i] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
+    }
+}
+
+
+// ------------------------------------------------------------------- K5
+// Non-increasing input (K1: no ascent): the stable sort is the reversal in
+// which every run of equal keys keeps its input order.  A run [a, b) of the
+// input lands at [n - b, n - a), so element i goes to n - b(i) + (i - a(i)).
+// Keys only: equal keys are indistinguishable, so out[n - 1 - i] = in[i] is
+// already exact (one read, one write, like the sorted-input copy).  With a
+// payload the run bounds matter: per 4096-key tile, k_rev_tile_bounds records
+// the last run start and the first run end in the tile, k_rev_carry scans
+// them across tiles (prefix max / suffix min), and k_rev_scatter finishes a(i)
+// and b(i) with block scans and moves keys and payload.  Every kernel returns at
+// once unless the plan chose this path (no host round trip; graph-capturable).
+constexpr int kRevTile = 4096, kRevBlock = 512, kRevPer = kRevTile / kRevBlock;
+
+template <typename K>
+__global__ void k_reverse_keys(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+                               const RadixState* __restrict__ st) {
+    if (!st->reversed) return;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[n - 1 - i] = in[i];
+}
+
+// run start / run end flags of position i (K >= 2 elements compared as keys)
+template <typename K>
+__device__ __forceinline__ bool rev_head(const K* keys, uint64_t i) { return i == 0 || keys[i - 1] != keys[i]; }
+template <typename K>
+__device__ __forceinline__ bool rev_end(const K* keys, uint64_t i, uint64_t n) {
+    return i + 1 == n || keys[i] != keys[i + 1];
+}
+
+// Per tile: the last run start in the tile (or -1) and the first run end (exclusive
+// index; INT64_MAX when no run ends in the tile).
+template <typename K>
+__global__ void __launch_bounds__(kRevBlock) k_rev_tile_bounds(const K* __restrict__ keys, uint64_t n,
+                                                              const RadixState* __restrict__ st,
+                                                              long long* __restrict__ last_head,
+                                                              long long* __restrict__ first_end) {
+    if (!st->reversed) return;
+    const uint64_t tiles = (n + kRevTile - 1) / kRevTile;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        long long h = -1, e = LLONG_MAX;
+        for (int j = 0; j < kRevPer; ++j) {
+            const uint64_t i = t * kRevTile + static_cast<uint64_t>(j) * kRevBlock + threadIdx.x;
+            if (i < n) {
+                if (rev_head(keys, i)) h = max(h, static_cast<long long>(i));
+                if (rev_end(keys, i, n)) e = min(e, static_cast<long long>(i) + 1);
+            }
+        }
+        h = block_reduce_max_ll<kRevBlock>(h);
+        e = -block_reduce_max_ll<kRevBlock>(-e);
+        if (threadIdx.x == 0) {
+            last_head[t] = h;
+            first_end[t] = e;
+        }
+    }
+}
+
+// One CTA: carry_head[t] = max(last_head[0..t-1]) and carry_end[t] =
+// min(first_end[t+1..]) in place of the inputs.
+__global__ void __launch_bounds__(1024) k_rev_carry(uint64_t n, const RadixState* __restrict__ st,
+                                                    long long* __restrict__ head, long long* __restrict__ end) {
+    if (!st->reversed) return;
+    const long long tiles = static_cast<long long>((n + kRevTile - 1) / kRevTile);
+    const long long per = (tiles + 1023) / 1024;
+    const long long lo = threadIdx.x * per, hi = min(tiles, lo + per);
+    long long hm = -1, em = LLONG_MAX;
+    for (long long t = lo; t < hi; ++t) hm = max(hm, head[t]);
+    for (long long t = lo; t < hi; ++t) em = min(em, end[t]);
+    __shared__ long long sh[1024], se[1024];
+    sh[threadIdx.x] = hm;
+    se[threadIdx.x] = em;
+    __syncthreads();
+    long long ph = -1, pe = LLONG_MAX;  // exclusive prefix max over threads < me / suffix min over threads > me
+    for (int k = 0; k < static_cast<int>(threadIdx.x); ++k) ph = max(ph, sh[k]);
+    for (int k = threadIdx.x + 1; k < 1024; ++k) pe = min(pe, se[k]);
+    __syncthreads();
+    for (long long t = lo; t < hi; ++t) {  // forward: exclusive prefix max
+        const long long v = head[t];
+        head[t] = ph;
+        ph = max(ph, v);
+    }
+    for (long long t = hi - 1; t >= lo; --t) {  // backward: exclusive suffix min
+        const long long v = end[t];
+        end[t] = pe;
+        pe = min(pe, v);
+    }
+}
+
+template <typename K, bool VALS>
+__global__ void __launch_bounds__(kRevBlock) k_rev_scatter(const K* __restrict__ kin, K* __restrict__ kout,
+                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
+                                                          int iota_vals, uint64_t n, const RadixState* __restrict__ st,
+                                                          const long long* __restrict__ carry_head,
+                                                          const long long* __restrict__ carry_end) {
+    if (!st->reversed) return;
+    __shared__ long long s_h[kRevBlock / 32], s_e[kRevBlock / 32];
+    const uint64_t tiles = (n + kRevTile - 1) / kRevTile;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        // thread owns positions [base, base + kRevPer) of the tile (blocked)
+        const uint64_t base = t * kRevTile + static_cast<uint64_t>(threadIdx.x) * kRevPer;
+        long long a[kRevPer], b[kRevPer];
+        long long run = -1;
+#pragma unroll
+        for (int j = 0; j < kRevPer; ++j) {
+            const uint64_t i = base + j;
+            if (i < n && rev_head(kin, i)) run = static_cast<long long>(i);
+            a[j] = run;  // -1: the run started before this thread's positions
+        }
+        long long eend = LLONG_MAX;
+#pragma unroll
+        for (int j = kRevPer - 1; j >= 0; --j) {
+            const uint64_t i = base + j;
+            if (i < n && rev_end(kin, i, n)) eend = static_cast<long long>(i) + 1;
+            b[j] = eend;  // LLONG_MAX: the run ends after this thread's positions
+        }
+        // block exclusive prefix max of the threads' last heads, suffix min of first ends
+        long long inc_h = a[kRevPer - 1], inc_e = b[0];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long th = __shfl_up_sync(ISORT_FULL_MASK, inc_h, o);
+            const long long te = __shfl_down_sync(ISORT_FULL_MASK, inc_e, o);
+            if (lane >= static_cast<uint32_t>(o)) inc_h = max(inc_h, th);
+            if (lane + o < 32) inc_e = min(inc_e, te);
+        }
+        __syncthreads();
+        if (lane == 31) s_h[warp] = inc_h;
+        if (lane == 0) s_e[warp] = inc_e;
+        __syncthreads();
+        long long ex_h = __shfl_up_sync(ISORT_FULL_MASK, inc_h, 1);
+        long long ex_e = __shfl_down_sync(ISORT_FULL_MASK, inc_e, 1);
+        if (lane == 0) ex_h = -1;
+        if (lane == 31) ex_e = LLONG_MAX;
+        for (uint32_t w = 0; w < warp; ++w) ex_h = max(ex_h, s_h[w]);
+        for (uint32_t w = warp + 1; w < kRevBlock / 32; ++w) ex_e = min(ex_e, s_e[w]);
+        ex_h = max(ex_h, carry_head[t]);
+        ex_e = min(ex_e, carry_end[t]);
+#pragma unroll
+        for (int j = 0; j < kRevPer; ++j) {
+            const uint64_t i = base + j;
+            if (i < n) {
+                const long long aa = a[j] >= 0 ? a[j] : ex_h;
+                const long long bb = b[j] != LLONG_MAX ? b[j] : ex_e;
+                const uint64_t p = n - static_cast<uint64_t>(bb) + (i - static_cast<uint64_t>(aa));
+                kout[p] = kin[i];
+                if (VALS) vout[p] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
+            }
+        }
     }
 }
 

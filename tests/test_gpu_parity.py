@@ -539,3 +539,45 @@ def test_key_range_protocol_single_rank_gpu(cuda, oracle):
         sk, sv, _ = KeyRangeSorter(OneRank(), CudaOps(torch.device("cuda:0"))).sort(tk, tv, algorithm=alg)
         assert np.array_equal(sk.cpu().numpy().view(np.uint32), want_k)
         assert np.array_equal(sv.cpu().numpy().view(np.uint32), want_i)
+
+
+# ------------------------------------------------------- reverse-sorted early-out (K1 ascents == 0)
+@pytest.mark.parametrize("n", [2, 3, 4095, 4096, 4097, 3 * 4096 + 1, 100_003, 1_000_000, 5_000_011])
+def test_reverse_sorted_early_out_is_stable(cuda, oracle, n):
+    """Non-increasing input takes the run-wise reversal instead of digit passes:
+    keys with runs of equal values (short runs, runs across 4096-key tiles, one
+    run of everything) must come out with their positions in input order."""
+    rng = np.random.default_rng(n)
+    cases = {
+        "distinct": np.sort(rng.choice(1 << 32, size=n, replace=False).astype(np.uint32))[::-1],
+        "short_runs": np.sort(rng.integers(0, max(2, n // 3), size=n, dtype=np.uint64).astype(np.uint32))[::-1],
+        "long_runs": np.sort(rng.integers(0, 5, size=n, dtype=np.uint64).astype(np.uint32))[::-1],
+        "constant": np.full(n, 7, dtype=np.uint32),
+    }
+    for name, k in cases.items():
+        k = np.ascontiguousarray(k)
+        want_k, want_i = oracle.sort_u32(k, with_index=True)
+        for alg in ("radix", "bucket"):
+            got_k, got_i = dev_sort(k, alg, "iota", range_bound=U32_MAX)
+            assert np.array_equal(got_k, want_k), (name, alg, n)
+            assert np.array_equal(got_i, want_i), (name, alg, n)
+            got_k, _ = dev_sort(k, alg, None, range_bound=U32_MAX)
+            assert np.array_equal(got_k, want_k), (name, alg, n, "keys only")
+        # a loaded payload follows its key
+        pay = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        import torch
+
+        from paper_1206_3511_b200 import device
+
+        s = device.Sorter(n, 4, "radix", "load")
+        ko, vo = s(torch.from_numpy(k.view(np.int32)).cuda(), torch.from_numpy(pay.view(np.int32)).cuda())
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), pay[want_i]), (name, n, "load")
+
+
+def test_one_ascent_takes_the_digit_passes(cuda, oracle):
+    k = np.sort(np.random.default_rng(3).integers(0, 1 << 32, size=50_000, dtype=np.uint64).astype(np.uint32))[::-1]
+    k = np.ascontiguousarray(k)
+    k[25_000], k[25_001] = k[25_001], k[25_000]  # one ascent: not non-increasing any more
+    want_k, want_i = oracle.sort_u32(k, with_index=True)
+    got_k, got_i = dev_sort(k, "radix", "iota")
+    assert np.array_equal(got_k, want_k) and np.array_equal(got_i, want_i)

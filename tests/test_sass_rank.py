@@ -1,0 +1,69 @@
+"""The one-sweep rank's stability rests on one instruction: a returning shared
+atomic add (SASS ATOMS.ADD) whose same-address lanes are granted in ascending
+lane order.  k_selftest_atomic_order re-checks that property at load time, so it
+must exercise the SAME instruction the rank compiles to.  This CPU test
+disassembles libisort.so (cuobjdump) and pins:
+  * the fast pass (SAFE = false) ranks with ATOMS.ADD and has no MATCH,
+  * the load-time self-test uses ATOMS.ADD (and MATCH.ANY as its reference),
+  * the fallback pass (SAFE = true) ranks with MATCH.ANY,
+  * the segment sort of the bucket path ranks with ATOMS.ADD too."""
+from __future__ import annotations
+
+import collections
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1206_3511_b200", "libisort.so")
+
+
+@pytest.fixture(scope="module")
+def sass_ops():
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-sass", LIB], capture_output=True, text=True, check=True).stdout
+    ops = collections.defaultdict(collections.Counter)
+    fn = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            fn = m.group(1)
+            continue
+        m = re.search(r"\b(ATOMS\.[A-Z0-9.]+|MATCH\.[A-Z]+)", line)
+        if m and fn:
+            ops[fn][m.group(1)] += 1
+    return ops
+
+
+def _find(ops, *parts):
+    hits = [f for f in ops if all(p in f for p in parts)]
+    assert hits, f"no kernel matching {parts}"
+    return hits
+
+
+def test_fast_rank_is_returning_shared_atomic(sass_ops):
+    # k_onesweep<u32, RadixDigitizer<u32>, 512, 24, 2, VALS=0, SAFE=0, SCATTER=0, LW>
+    for f in _find(sass_ops, "k_onesweep", "RadixDigitizerIj", "Li512ELi24ELi2ELb0ELb0ELb0E"):
+        c = sass_ops[f]
+        assert c["ATOMS.ADD"] > 0, f
+        assert not any(k.startswith("MATCH") for k in c), f
+
+
+def test_selftest_checks_the_same_instruction(sass_ops):
+    (f,) = _find(sass_ops, "k_selftest_atomic_order")
+    assert sass_ops[f]["ATOMS.ADD"] > 0 and sass_ops[f]["MATCH.ANY"] > 0
+
+
+def test_safe_rank_uses_match(sass_ops):
+    for f in _find(sass_ops, "k_onesweep", "RadixDigitizerIj", "Li512ELi24ELi2ELb0ELb1ELb0E"):
+        assert sass_ops[f]["MATCH.ANY"] > 0, f
+
+
+def test_segment_sort_rank(sass_ops):
+    for f in _find(sass_ops, "k_bucket_segments"):
+        assert sass_ops[f]["ATOMS.ADD"] > 0, f

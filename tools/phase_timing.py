@@ -43,8 +43,8 @@ import ctypes as C
 
 class RadixState(C.Structure):
     _fields_ = [("hist", C.c_uint32 * 2048), ("offs", C.c_uint32 * 2048), ("max_key", C.c_uint64),
-                ("first_bad", C.c_uint64), ("descents", C.c_uint32),
-                ("n_active", C.c_uint32), ("copy_in_to_out", C.c_uint32), ("tile_ticket", C.c_uint32 * 8),
+                ("first_bad", C.c_uint64), ("descents", C.c_uint32), ("ascents", C.c_uint32),
+                ("n_active", C.c_uint32), ("copy_in_to_out", C.c_uint32), ("reversed", C.c_uint32), ("tile_ticket", C.c_uint32 * 8),
                 ("digit_of_slot", C.c_int32 * 8), ("src_of_slot", C.c_int32 * 8), ("dst_of_slot", C.c_int32 * 8),
                 ("prof", C.c_uint64 * 16)]
 
