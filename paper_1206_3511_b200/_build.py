@@ -25,7 +25,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-O3", "-shared",
-    "-split-compile=0",  # device optimisation in parallel threads (the kernel templates dominate the build)
+    # (no -split-compile: measured 62.8 vs 81.3 Gkeys/s for the radix sort -- it changes the kernels' code)
 ]
 
 

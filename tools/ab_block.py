@@ -22,7 +22,9 @@ vout = torch.empty(n, dtype=torch.int32, device="cuda") if mode else None
 for so in sys.argv[1:]:
     lib = ctypes.CDLL(os.path.abspath(so))
     for name, (res, args) in _lib.SIGNATURES.items():
-        f = getattr(lib, name)
+        f = getattr(lib, name, None)  # older builds lack newer entry points
+        if f is None:
+            continue
         f.restype, f.argtypes = res, args
     tb = lib.isort_radix_temp_bytes(n, 8 if k64 else 4, mode)
     sortfn = lib.isort_radix_sort_u64 if k64 else lib.isort_radix_sort_u32

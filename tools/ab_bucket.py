@@ -20,7 +20,9 @@ for so in sys.argv[1:]:
     for name, (res, args) in _lib.SIGNATURES.items():
         if not hasattr(lib, name):  # older builds: entry points added since
             continue
-        f = getattr(lib, name)
+        f = getattr(lib, name, None)  # older builds lack newer entry points
+        if f is None:
+            continue
         f.restype, f.argtypes = res, args
     tb = lib.isort_bucket_temp_bytes(n, 4, 0)
     temp = torch.empty(tb, dtype=torch.uint8, device="cuda")
