@@ -8,6 +8,7 @@
 // sort, gather of whole records by position, D2H.  No CPU fallback exists.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -478,17 +479,18 @@ struct DevBuf {
     }
 };
 
-__global__ void k_pack_records_u32(const isort_record* __restrict__ rec, uint32_t* __restrict__ keys, uint64_t n,
+// Packs records [lo, lo + m) into SoA u32 keys (low 32 bits) and folds the max key.
+__global__ void k_pack_records_u32(const isort_record* __restrict__ rec, uint32_t* __restrict__ keys, uint64_t m,
                                    unsigned long long* __restrict__ max_key) {
-    unsigned long long m = 0;
+    unsigned long long mx = 0;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
         const uint64_t k = rec[i].key;
         keys[i] = static_cast<uint32_t>(k);
-        m = k > m ? k : m;
+        mx = k > mx ? k : mx;
     }
-    m = warp_max<unsigned long long>(m);
-    if (lane_id() == 0 && m) atomicMax(max_key, m);
+    mx = warp_max<unsigned long long>(mx);
+    if (lane_id() == 0 && mx) atomicMax(max_key, mx);
 }
 
 __global__ void k_pack_records_u64(const isort_record* __restrict__ rec, uint64_t* __restrict__ keys, uint64_t n) {
@@ -504,9 +506,147 @@ __global__ void k_gather_records(const isort_record* __restrict__ in, const uint
         out[i] = in[idx[i]];
 }
 
+// ------------------------------------------------ staged host <-> device transfers
+// The drop-in's records live in pageable host memory (std::vector, record.hpp:27-30).
+// A plain cudaMemcpy from pageable memory runs at a fraction of PCIe speed and
+// cannot overlap anything.  Instead T worker threads each take every T-th chunk,
+// copy it into one of their two pinned staging slots (library-owned, reused
+// across calls) and issue its DMA on their own stream, so host copies, PCIe
+// transfers in both directions and per-chunk device work (the key pack) overlap.
+constexpr size_t kStageChunk = 16u << 20;  // bytes per chunk (a multiple of 16 B records)
+constexpr int kStageSlots = 2;             // per worker
 
-// Sort records by key through the device: pack -> (key, position) sort -> gather.
-// `sorter(keys_in, keys_out, idx_out, n, s)` is called with u32 or u64 keys.
+struct Staging {
+    std::mutex mu;  // one transfer per device at a time
+    int workers = 0;
+    std::vector<cudaStream_t> streams;
+    std::vector<void*> slots;           // workers * kStageSlots pinned buffers
+    std::vector<cudaEvent_t> slot_done;  // the slot's last DMA finished
+    std::vector<cudaEvent_t> done;       // per worker: all its work queued so far
+};
+Staging g_staging[64];
+
+int staging_for(int dev, Staging** out) {
+    Staging& st = g_staging[dev & 63];
+    if (st.workers == 0) {
+        int w = static_cast<int>(std::thread::hardware_concurrency());
+        w = w >= 16 ? 8 : (w >= 4 ? w / 2 : 1);
+        if (const char* e = std::getenv("ISORT_STAGING_THREADS")) w = std::max(1, std::atoi(e));
+        for (int i = 0; i < w; ++i) {
+            cudaStream_t sw;
+            cudaEvent_t ev;
+            ISORT_CUDA_TRY(cudaStreamCreateWithFlags(&sw, cudaStreamNonBlocking));
+            ISORT_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            st.streams.push_back(sw);
+            st.done.push_back(ev);
+            for (int k = 0; k < kStageSlots; ++k) {
+                void* p = nullptr;
+                ISORT_CUDA_TRY(cudaHostAlloc(&p, kStageChunk, cudaHostAllocPortable));
+                cudaEvent_t se;
+                ISORT_CUDA_TRY(cudaEventCreateWithFlags(&se, cudaEventDisableTiming));
+                st.slots.push_back(p);
+                st.slot_done.push_back(se);
+            }
+        }
+        st.workers = w;
+    }
+    *out = &st;
+    return ISORT_OK;
+}
+
+// Runs fn(worker) on every worker thread (worker 0 on the calling thread); the
+// first non-zero return code wins.
+template <typename Fn>
+int run_workers(int workers, Fn&& fn) {
+    std::vector<int> rcs(workers, ISORT_OK);
+    std::vector<std::thread> th;
+    for (int w = 1; w < workers; ++w) th.emplace_back([&, w] { rcs[w] = fn(w); });
+    rcs[0] = fn(0);
+    for (auto& t : th) t.join();
+    for (int rc : rcs)
+        if (rc) return rc;
+    return ISORT_OK;
+}
+
+// Pageable host -> device.  after(w_stream, offset, len) queues per-chunk device
+// work behind the chunk's DMA.  The main stream `s` is made to wait for all of it.
+template <typename After>
+int upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s, Staging& st, After&& after) {
+    const size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+    cudaEvent_t start;
+    ISORT_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    cudaEventRecord(start, s);  // dst was allocated stream-ordered on s
+    const int dev = [] { int d = 0; cudaGetDevice(&d); return d; }();
+    int rc = run_workers(st.workers, [&](int w) -> int {
+        cudaSetDevice(dev);
+        cudaStream_t ws = st.streams[w];
+        ISORT_CUDA_TRY(cudaStreamWaitEvent(ws, start, 0));
+        int k = 0;
+        for (size_t c = static_cast<size_t>(w); c < chunks; c += static_cast<size_t>(st.workers), k ^= 1) {
+            const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+            const int slot = w * kStageSlots + k;
+            ISORT_CUDA_TRY(cudaEventSynchronize(st.slot_done[slot]));  // its previous DMA has read it
+            std::memcpy(st.slots[slot], static_cast<const char*>(src) + off, len);
+            ISORT_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.slots[slot], len,
+                                           cudaMemcpyHostToDevice, ws));
+            ISORT_CUDA_TRY(cudaEventRecord(st.slot_done[slot], ws));
+            if (int r = after(ws, off, len)) return r;
+        }
+        ISORT_CUDA_TRY(cudaEventRecord(st.done[w], ws));
+        return ISORT_OK;
+    });
+    cudaEventDestroy(start);
+    if (rc) return rc;
+    for (int w = 0; w < st.workers; ++w) ISORT_CUDA_TRY(cudaStreamWaitEvent(s, st.done[w], 0));
+    return ISORT_OK;
+}
+
+// Device -> pageable host, after everything queued on `s` so far.  Synchronous.
+int download_staged(void* dst, const void* src, size_t bytes, cudaStream_t s, Staging& st) {
+    const size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+    cudaEvent_t ready;
+    ISORT_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    ISORT_CUDA_TRY(cudaEventRecord(ready, s));
+    const int dev = [] { int d = 0; cudaGetDevice(&d); return d; }();
+    int rc = run_workers(st.workers, [&](int w) -> int {
+        cudaSetDevice(dev);
+        cudaStream_t ws = st.streams[w];
+        ISORT_CUDA_TRY(cudaStreamWaitEvent(ws, ready, 0));
+        // two slots in flight: chunk j's DMA overlaps the host copy-out of chunk j - 1
+        size_t prev_off = 0, prev_len = 0;
+        int prev_slot = -1, k = 0;
+        for (size_t c = static_cast<size_t>(w);; c += static_cast<size_t>(st.workers), k ^= 1) {
+            const bool more = c < chunks;
+            int slot = -1;
+            size_t off = 0, len = 0;
+            if (more) {
+                off = c * kStageChunk;
+                len = std::min(kStageChunk, bytes - off);
+                slot = w * kStageSlots + k;
+                ISORT_CUDA_TRY(cudaMemcpyAsync(st.slots[slot], static_cast<const char*>(src) + off, len,
+                                               cudaMemcpyDeviceToHost, ws));
+                ISORT_CUDA_TRY(cudaEventRecord(st.slot_done[slot], ws));
+            }
+            if (prev_slot >= 0) {
+                ISORT_CUDA_TRY(cudaEventSynchronize(st.slot_done[prev_slot]));
+                std::memcpy(static_cast<char*>(dst) + prev_off, st.slots[prev_slot], prev_len);
+            }
+            if (!more) break;
+            prev_slot = slot;
+            prev_off = off;
+            prev_len = len;
+        }
+        return ISORT_OK;
+    });
+    cudaEventDestroy(ready);
+    return rc;
+}
+
+// Sort records by key through the device: staged H2D with the key pack per chunk
+// -> (key, position) sort -> gather -> staged D2H.  `sort32/sort64(keys_in,
+// keys_out, idx_out, n, s)` run the u32 / u64 pipelines.  One host read per call:
+// the max key after the upload decides u32 or u64 keys (the sort cannot start
+// before the last chunk has arrived anyway).
 template <typename Sort32, typename Sort64>
 int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t n, int device, Sort32&& sort32,
                             Sort64&& sort64) {
@@ -516,34 +656,46 @@ int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t 
     if (n > kMaxLookbackN)
         return set_error(ISORT_ERANGE, "n=%llu exceeds the per-call limit %llu", (unsigned long long)n,
                          (unsigned long long)kMaxLookbackN);
+    Staging* stg = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_pool_mu);  // creation of the per-device staging
+        if ((rc = staging_for(device, &stg))) return rc;
+    }
+    std::lock_guard<std::mutex> g(stg->mu);
     DevBuf rec_in, rec_out, keys, keys_out, idx, maxw;
     if ((rc = rec_in.alloc(n * sizeof(isort_record), s)) || (rc = rec_out.alloc(n * sizeof(isort_record), s)) ||
         (rc = keys.alloc(n * sizeof(uint64_t), s)) || (rc = keys_out.alloc(n * sizeof(uint64_t), s)) ||
         (rc = idx.alloc(n * sizeof(uint32_t), s)) || (rc = maxw.alloc(sizeof(unsigned long long), s)))
         return rc;
-    ISORT_CUDA_TRY(cudaMemcpyAsync(rec_in.p, in, n * sizeof(isort_record), cudaMemcpyHostToDevice, s));
     ISORT_CUDA_TRY(cudaMemsetAsync(maxw.p, 0, sizeof(unsigned long long), s));
-    k_pack_records_u32<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), keys.as<uint32_t>(), n,
-                                                  maxw.as<unsigned long long>());
+    auto* rin = rec_in.as<isort_record>();
+    auto* k32 = keys.as<uint32_t>();
+    auto* mxp = maxw.as<unsigned long long>();
+    rc = upload_staged(rin, in, n * sizeof(isort_record), s, *stg, [&](cudaStream_t ws, size_t off, size_t len) {
+        const uint64_t lo = off / sizeof(isort_record), m = len / sizeof(isort_record);
+        k_pack_records_u32<<<grid_for(m), 256, 0, ws>>>(rin + lo, k32 + lo, m, mxp);
+        launched();
+        return cudaGetLastError() == cudaSuccess ? ISORT_OK : set_error(ISORT_ECUDA, "k_pack_records_u32 launch");
+    });
+    if (rc) return rc;
     unsigned long long mx = 0;
     ISORT_CUDA_TRY(cudaMemcpyAsync(&mx, maxw.p, sizeof mx, cudaMemcpyDeviceToHost, s));
     ISORT_CUDA_TRY(cudaStreamSynchronize(s));
     if (mx <= 0xffffffffull) {
-        rc = sort32(keys.as<uint32_t>(), keys_out.as<uint32_t>(), idx.as<uint32_t>(), n, s);
+        rc = sort32(k32, keys_out.as<uint32_t>(), idx.as<uint32_t>(), n, s);
     } else {
-        k_pack_records_u64<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), keys.as<uint64_t>(), n);
+        k_pack_records_u64<<<grid_for(n), 256, 0, s>>>(rin, keys.as<uint64_t>(), n);
+        launched();
         rc = sort64(keys.as<uint64_t>(), keys_out.as<uint64_t>(), idx.as<uint32_t>(), n, s);
     }
     if (rc) {
         cudaStreamSynchronize(s);
         return rc;
     }
-    k_gather_records<<<grid_for(n), 256, 0, s>>>(rec_in.as<isort_record>(), idx.as<uint32_t>(),
-                                                rec_out.as<isort_record>(), n);
+    k_gather_records<<<grid_for(n), 256, 0, s>>>(rin, idx.as<uint32_t>(), rec_out.as<isort_record>(), n);
+    launched();
     ISORT_CUDA_TRY(cudaGetLastError());
-    ISORT_CUDA_TRY(cudaMemcpyAsync(out, rec_out.p, n * sizeof(isort_record), cudaMemcpyDeviceToHost, s));
-    ISORT_CUDA_TRY(cudaStreamSynchronize(s));
-    return ISORT_OK;
+    return download_staged(out, rec_out.p, n * sizeof(isort_record), s, *stg);
 }
 
 template <typename K>

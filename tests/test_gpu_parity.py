@@ -581,3 +581,15 @@ def test_one_ascent_takes_the_digit_passes(cuda, oracle):
     want_k, want_i = oracle.sort_u32(k, with_index=True)
     got_k, got_i = dev_sort(k, "radix", "iota")
     assert np.array_equal(got_k, want_k) and np.array_equal(got_i, want_i)
+
+
+# ------------------------------------------------------- Records drop-in: staged multi-chunk transfers
+@pytest.mark.parametrize("n,bits", [(3_000_001, 32), (2_500_003, 40), (1_048_576, 20)])
+def test_records_staged_transfer_many_chunks(cuda, oracle, n, bits):
+    """radix_sort_lsd / bucket_sort on Records big enough to span many 16 MB
+    staging chunks and every transfer worker (u32 and u64 key paths)."""
+    rng = np.random.default_rng(n)
+    seq = recs(rng.integers(0, 1 << bits, size=n, dtype=np.uint64))
+    want = oracle.radix_sort_lsd(seq, 256)
+    assert np.array_equal(isort.radix_sort_lsd(seq, 256), want)
+    assert np.array_equal(isort.bucket_sort(seq, (1 << bits) - 1), want)
