@@ -24,9 +24,11 @@ REFERENCE = "/root/reference/proj"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O3", "-shared",
-    # (no -split-compile: measured 62.8 vs 81.3 Gkeys/s for the radix sort -- it changes the kernels' code)
+    "-Xcompiler", "-fPIC,-O3",
+    # (no -split-compile: measured 62.8 vs 81.3 Gkeys/s for the radix sort -- it changes the kernels' code;
+    #  the kernels are split across translation units instead, see csrc/isort_launch.cuh)
 ]
+OBJ_DIR = os.path.join(PKG, "build")
 
 
 def _nvcc() -> str:
@@ -43,12 +45,33 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build_engine(force: bool = False, verbose: bool = False) -> str:
+def build_engine(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    """Compile every translation unit of csrc/ to an object (in parallel: ptxas
+    is single-threaded per unit), then link libisort.so.  --no-undefined makes a
+    missing explicit instantiation a build error rather than a load error."""
+    from concurrent.futures import ThreadPoolExecutor
+
     units = sorted(glob.glob(os.path.join(CSRC, "*.cu")))  # translation units of libisort.so
-    sources = sorted(units + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
                      + [os.path.join(ROOT, "include", "isort.h")])
-    if force or _stale(LIB, sources):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *units]
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = [os.path.join(OBJ_DIR, os.path.basename(u)[:-3] + ".o") for u in units]
+    todo = [(u, o) for u, o in zip(units, objs) if force or _stale(o, [u] + headers)]
+
+    def compile_one(uo):
+        u, o = uo
+        cmd = [_nvcc(), *NVCC_FLAGS, "-c", "-o", o + ".tmp", u]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        os.replace(o + ".tmp", o)
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
+            list(ex.map(compile_one, todo))
+    if force or todo or _stale(LIB, objs):
+        cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker", "--no-undefined",
+               "-o", LIB + ".tmp", *objs]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True, cwd=CSRC)

@@ -764,7 +764,7 @@ struct DestDigitizer {
     __device__ __forceinline__ bool in_range(K) const { return true; }
 };
 
-__global__ void k_copy_part_counts(const RadixState* __restrict__ st, uint64_t* __restrict__ counts, int parts) {
+static __global__ void k_copy_part_counts(const RadixState* __restrict__ st, uint64_t* __restrict__ counts, int parts) {
     if (threadIdx.x < parts) counts[threadIdx.x] = st->hist[0][threadIdx.x];
 }
 

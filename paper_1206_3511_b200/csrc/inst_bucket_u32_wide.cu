@@ -1,0 +1,13 @@
+// inst_bucket_u32_wide.cu -- explicit instantiations of the bucket-sort (u32 keys, kWide bucket index) launch templates
+// (isort_launch.cuh): one translation unit per key type / digitizer family so the
+// kernels compile in parallel.
+#define ISORT_LAUNCH_DEFINITIONS
+#include "isort_launch.cuh"
+
+namespace isort {
+using BDz = BucketDigitizer<uint32_t, kWide>;
+ISORT_INST_PIPELINE(uint32_t, false, BDz)
+ISORT_INST_PIPELINE(uint32_t, true, BDz)
+ISORT_INST_SEGMENTS(uint32_t, BDz, false)
+ISORT_INST_SEGMENTS(uint32_t, BDz, true)
+}  // namespace isort

@@ -29,6 +29,7 @@
 #include "isort_common.cuh"
 #include "isort_internal.h"
 #include "radix_onesweep.cuh"
+#include "isort_launch.cuh"
 
 namespace isort {
 
@@ -62,7 +63,7 @@ struct ProfSink {
 thread_local ProfSink g_prof;
 
 
-inline void prof_mark(cudaStream_t s, const char* name) {
+void prof_mark(cudaStream_t s, const char* name) {
     if (!g_prof.on) return;
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
@@ -71,63 +72,6 @@ inline void prof_mark(cudaStream_t s, const char* name) {
     g_prof.names.emplace_back(name);
 }
 
-// ----------------------------------------------------- kernel configuration
-// Tile shapes per (key width, payload).  Tile = BLOCK * IPT keys.
-#ifndef ISORT_PASS_BLOCK
-#define ISORT_PASS_BLOCK 512
-#endif
-// One-sweep tile shape: BLOCK threads x IPT keys per chunk, CHUNKS chunks per
-// tile.  Large inputs use 2 chunks of 24 keys per thread (DESIGN.md 3.1 has the
-// sweep); inputs below kSmallN use one 8,192-key chunk per tile so a few million
-// keys still fill all SMs (raising the threshold to 16M or 32M measured no gain).
-#ifndef ISORT_SMALL_N
-#define ISORT_SMALL_N (4ull << 20)
-#endif
-constexpr uint64_t kSmallN = ISORT_SMALL_N;
-
-#ifndef ISORT_PASS_CHUNKS
-#define ISORT_PASS_CHUNKS 2
-#endif
-template <typename K, bool VALS, int CHUNKS = ISORT_PASS_CHUNKS>
-struct PassCfg {
-    static constexpr int kBlock = ISORT_PASS_BLOCK;
-#ifndef ISORT_PASS_IPT32
-#define ISORT_PASS_IPT32 24
-#endif
-#ifndef ISORT_PASS_IPT32V
-#define ISORT_PASS_IPT32V 12
-#endif
-#ifndef ISORT_PASS_IPT64
-#define ISORT_PASS_IPT64 12
-#endif
-    // keys per thread per chunk; the 1-chunk small-n tile: 16 (1M keys: 51 us vs 57 with 12, 53 with 24)
-#ifndef ISORT_PASS_IPT_SMALL
-#define ISORT_PASS_IPT_SMALL 16
-#endif
-    static constexpr int kIpt = sizeof(K) == 4 ? (VALS ? ISORT_PASS_IPT32V : (CHUNKS == 1 ? ISORT_PASS_IPT_SMALL : ISORT_PASS_IPT32))
-                                               : (VALS ? 6 : ISORT_PASS_IPT64);
-    static constexpr int kChunks = CHUNKS;
-    static constexpr int kTile = kBlock * kIpt * kChunks;
-    static constexpr int kCtasPerSm = ISORT_PASS_MINB_OF(kBlock);
-};
-
-template <typename K, bool VALS>
-inline int pass_tile(uint64_t n) {
-    return n < kSmallN ? PassCfg<K, VALS, 1>::kTile : PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
-}
-
-// Upfront histogram replication (lane copies per bin): 64 KB of counters.
-template <int D>
-#ifndef ISORT_UF_REP
-#define ISORT_UF_REP 32
-#endif
-#ifndef ISORT_UF_BLOCK
-#define ISORT_UF_BLOCK 1024
-#endif
-struct UpfrontCfg {
-    static constexpr int kRep = D <= 4 ? ISORT_UF_REP : 8;
-    static constexpr size_t kSmem = static_cast<size_t>(D) * kRadix * kRep * sizeof(uint32_t);
-};
 
 // ------------------------------------------------------- rank self-test
 // The fast one-sweep rank relies on same-address shared atomics of one warp
@@ -189,6 +133,7 @@ int rank_state() {
     return r;
 }
 bool rank_fast_path_ok() { return rank_state() == 1; }
+void prof_state(const RadixState* st) { g_prof.st = st; }
 
 std::atomic<int> g_sm_count[64];
 
@@ -207,10 +152,6 @@ int isort::sm_count() {
 
 namespace isort {
 
-constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
-
-// Bytes per look-back status word for a call over n keys (radix_onesweep.cuh).
-inline size_t lb_word_bytes(uint64_t n) { return n <= kNarrowLbMaxN ? 4 : 8; }
 
 struct RadixLayout {
     size_t state = 0, lookback = 0, keys_alt = 0, vals_alt = 0, total = 0;
@@ -246,11 +187,10 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
 std::mutex g_smem_mu;
 std::set<std::pair<const void*, int>> g_smem_done;
 
-template <typename F>
-void set_max_smem_once(F* kernel, size_t bytes) {
+void set_max_smem_once_raw(const void* kernel, size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    const auto key = std::make_pair(kernel, dev);
     std::lock_guard<std::mutex> g(g_smem_mu);
     if (g_smem_done.count(key)) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
@@ -260,11 +200,10 @@ void set_max_smem_once(F* kernel, size_t bytes) {
 // CTAs of `kernel` resident per SM (occupancy API), once per (kernel, device).
 std::map<std::pair<const void*, int>, int> g_occ;
 
-template <typename F>
-int resident_per_sm(F* kernel, int block, size_t smem) {
+int resident_per_sm_raw(const void* kernel, int block, size_t smem) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    const auto key = std::make_pair(kernel, dev);
     std::lock_guard<std::mutex> g(g_smem_mu);
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
@@ -275,102 +214,6 @@ int resident_per_sm(F* kernel, int block, size_t smem) {
     return per_sm;
 }
 
-template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false>
-void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
-                   uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
-                   const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{}) {
-    constexpr int D = Dz::kDigits;
-    using Smem = OnesweepSmem<K, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, !Dz::kCheapDigit>;
-    using Narrow = uint32_t;            // look-back status words: n < 2^30
-    using Wide = unsigned long long;    // n up to 2^32 - 1
-    const bool fast = rank_fast_path_ok();
-    const bool narrow = lb_word_bytes(n) == 4;
-    auto* kern = fast ? (narrow ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER, Narrow>
-                                : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, false, SCATTER, Wide>)
-                      : (narrow ? k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER, Narrow>
-                                : k_onesweep<K, Dz, Cfg::kBlock, Cfg::kIpt, Cfg::kChunks, VALS, true, SCATTER, Wide>);
-    set_max_smem_once(kern, sizeof(Smem));
-    const unsigned grid3 = tiles < static_cast<uint32_t>(Cfg::kCtasPerSm * sm_count()) ? tiles
-                                                                                     : Cfg::kCtasPerSm * sm_count();
-    for (int slot = 0; slot < D; ++slot) {
-        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
-                                                        tiles, slot, dz, scat);
-        static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
-                                                     "pass4", "pass5", "pass6", "pass7"};
-        prof_mark(s, kPassNames[slot]);
-    }
-}
-
-// Histogram step of a pipeline: zero the state, K1 (all digit histograms, max,
-// sortedness, range check), K2 (scans + pass plan).
-template <typename K, typename Dz>
-int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz,
-                     int plan_flags, bool zero_state, cudaStream_t s) {
-    constexpr int D = Dz::kDigits;
-    prof_mark(s, "start");
-    g_prof.st = st;
-    if (zero_state) {
-        const size_t bytes = reinterpret_cast<char*>(lookback) - reinterpret_cast<char*>(st) +
-                             static_cast<size_t>(D) * tiles * kRadix * lb_word_bytes(n);
-        ISORT_CUDA_TRY(cudaMemsetAsync(st, 0, bytes, s));
-        prof_mark(s, "memset");
-    }
-    const bool vec = (reinterpret_cast<uintptr_t>(kin) & 15u) == 0;
-    using UCfg = UpfrontCfg<D>;
-    const uint64_t want = (n + 4ull * kUpfrontBlock - 1) / (4ull * kUpfrontBlock);
-    auto* k1 = vec ? k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, true> : k_upfront<K, Dz, kUpfrontBlock, UCfg::kRep, false>;
-    set_max_smem_once(k1, UCfg::kSmem);
-    const uint64_t cap1 = static_cast<uint64_t>(resident_per_sm(k1, kUpfrontBlock, UCfg::kSmem)) * sm_count();
-    const unsigned grid1 = static_cast<unsigned>(want < cap1 ? (want ? want : 1) : cap1);
-    k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
-    prof_mark(s, "upfront");
-    k_plan<D><<<1, kRadix, 0, s>>>(st, n, plan_flags);
-    prof_mark(s, "plan");
-    launched(2);
-    ISORT_CUDA_TRY(cudaGetLastError());
-    return ISORT_OK;
-}
-
-// Launch the whole radix pipeline for digitizer `dz` (radix digits, or the
-// bucket sort's bucket-index digits).  Buffers: kin (const) -> kout, with kalt
-// as ping-pong; the plan decides which passes run.
-template <typename K, bool VALS, typename Dz>
-int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
-                          uint32_t* valt, bool iota, uint64_t n, RadixState* st, void* lookback,
-                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
-                          cudaStream_t s) {
-    constexpr int D = Dz::kDigits;
-    int rc = launch_histogram<K, Dz>(kin, n, st, lookback, tiles, dz, skip_sorted ? kPlanSkipSorted : 0, zero_state, s);
-    if (rc) return rc;
-
-    if (n < kSmallN)
-        launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
-                                                        dz, s);
-    else
-        launch_passes<K, VALS, Dz, PassCfg<K, VALS, ISORT_PASS_CHUNKS>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
-                                                        dz, s);
-    launched(D);
-    const uint64_t cblocks = (n + 4095) / 4096;
-    const unsigned cgrid = static_cast<unsigned>(cblocks < 4ull * sm_count() ? (cblocks ? cblocks : 1) : 4ull * sm_count());
-    k_copy_if_unsorted_skip<K><<<cgrid, 512, 0, s>>>(kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
-    prof_mark(s, "copy");
-    // non-increasing input (the plan's reverse early-out): the run-wise reversal
-    if (!VALS) {
-        k_reverse_keys<K><<<cgrid, 512, 0, s>>>(kin, kout, n, st);
-        launched(2);
-    } else {
-        auto* head = static_cast<long long*>(lookback);  // the look-back rows are unused on this path
-        auto* end = head + (n + kRevTile - 1) / kRevTile;
-        const unsigned rgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
-        k_rev_tile_bounds<K><<<rgrid, kRevBlock, 0, s>>>(kin, n, st, head, end);
-        k_rev_carry<<<1, 1024, 0, s>>>(n, st, head, end);
-        k_rev_scatter<K, true><<<rgrid, kRevBlock, 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st, head, end);
-        launched(4);
-    }
-    prof_mark(s, "reverse");
-    ISORT_CUDA_TRY(cudaGetLastError());
-    return ISORT_OK;
-}
 
 template <typename K>
 int radix_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout, uint64_t n, int vmode,
@@ -766,22 +609,6 @@ __global__ void k_is_sorted_u32(const uint32_t* __restrict__ keys, uint64_t n, u
 }
 
 
-// ------------------------------------------------------------- bucket sort
-#ifndef ISORT_SEG_BLOCK
-#define ISORT_SEG_BLOCK 512
-#endif
-#ifndef ISORT_SEG_IPT
-#define ISORT_SEG_IPT 32
-#endif
-constexpr int kSegBlock = ISORT_SEG_BLOCK;
-// keys per thread of a segment-sort stage (the stage lives in registers between
-// a pass's count and scatter): 32 for u32 keys (a 16,384-key stage; bigger
-// stages amortise the per-stage barriers -- 8,192 / 10,240 / 16,384 / 18,432 keys
-// measured 73.5 / 77.4 / 83.5 / 83.8 Gkeys/s), fewer with a payload or u64 keys
-template <typename K, bool VALS>
-constexpr int seg_ipt() {
-    return sizeof(K) == 4 ? (VALS ? 20 : ISORT_SEG_IPT) : (VALS ? 12 : 16);
-}
 
 struct BucketLayout {
     RadixLayout r;
@@ -799,20 +626,6 @@ BucketLayout bucket_layout(uint64_t n, bool vals) {
     return L;
 }
 
-// K5 launch: persistent, as many CTAs as fit (at most one per ~4K keys).
-template <typename K, typename Dz, bool VALS>
-void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, BucketState* bst, const Dz& dz,
-                     cudaStream_t s) {
-    constexpr int kSegIpt = seg_ipt<K, VALS>();
-    using Smem = SegSmem<K, kSegBlock, kSegIpt, VALS>;
-    static_assert(sizeof(Smem) <= 232448, "segment stage exceeds shared memory");
-    auto* kern = k_bucket_segments<K, Dz, kSegBlock, kSegIpt, VALS>;
-    set_max_smem_once(kern, sizeof(Smem));
-    const int per_sm = resident_per_sm(kern, kSegBlock, sizeof(Smem));
-    const uint64_t want = (n + kSegBlock * kSegIpt / 2 - 1) / (kSegBlock * kSegIpt / 2);
-    const uint64_t cap = static_cast<uint64_t>(per_sm) * sm_count();
-    kern<<<static_cast<unsigned>(want < cap ? want : cap), kSegBlock, sizeof(Smem), s>>>(keys, vals, n, st, bst, dz);
-}
 
 // After the pipeline: report a range error like the reference, or re-sort the
 // span of non-constant oversized super-buckets with the radix pipeline.

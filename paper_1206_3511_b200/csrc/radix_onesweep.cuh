@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
 // Load-time check of the property the fast rank relies on: lanes of one warp
 // instruction that add to the same shared word observe old values in ascending
 // lane order.  Adversarial patterns: 1..32 distinct words per instruction.
-__global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations, uint32_t seed) {
+static __global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations, uint32_t seed) {
     __shared__ uint32_t h[32][257];
     uint32_t* wh = h[threadIdx.x >> 5];
     const uint32_t lane = lane_id();
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(kRevBlock) k_rev_tile_bounds(const K* __restri
 
 // One CTA: carry_head[t] = max(last_head[0..t-1]) and carry_end[t] =
 // min(first_end[t+1..]) in place of the inputs.
-__global__ void __launch_bounds__(1024) k_rev_carry(uint64_t n, const RadixState* __restrict__ st,
+static __global__ void __launch_bounds__(1024) k_rev_carry(uint64_t n, const RadixState* __restrict__ st,
                                                     long long* __restrict__ head, long long* __restrict__ end) {
     if (!st->reversed) return;
     const long long tiles = static_cast<long long>((n + kRevTile - 1) / kRevTile);

@@ -593,3 +593,72 @@ def test_records_staged_transfer_many_chunks(cuda, oracle, n, bits):
     want = oracle.radix_sort_lsd(seq, 256)
     assert np.array_equal(isort.radix_sort_lsd(seq, 256), want)
     assert np.array_equal(isort.bucket_sort(seq, (1 << bits) - 1), want)
+
+
+# ------------------------------------------------------- host C-ABI entry points (the bench's e2e path)
+@pytest.mark.parametrize("n", [0, 1, 4097, 1_000_003])
+def test_host_entry_points_bit_exact(cuda, oracle, n):
+    """isort_radix_sort_host_u32 / isort_bucket_sort_host_u32: host keys in,
+    host keys out (bench.py's e2e call), bit-exact against the oracle, for
+    pageable and pinned host buffers."""
+    import ctypes
+
+    import torch
+
+    from paper_1206_3511_b200 import _lib
+
+    lib = _lib.load()
+    keys = oracle.uniform_u32(n, 7) if n else np.empty(0, dtype=np.uint32)
+    want = oracle.sort_u32(keys) if n else keys
+    for pinned in (False, True):
+        if pinned:
+            hin = torch.from_numpy(keys.view(np.int32).copy()).pin_memory()
+            hout = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
+            pin_, pout = hin.data_ptr() if n else None, hout.data_ptr()
+            got = lambda: hout.numpy()[:n].view(np.uint32)  # noqa: E731
+        else:
+            src = np.ascontiguousarray(keys)
+            dst = np.zeros(max(n, 1), dtype=np.uint32)
+            pin_, pout = src.ctypes.data_as(ctypes.c_void_p).value, dst.ctypes.data
+            got = lambda: dst[:n]  # noqa: E731
+        _lib.check(lib.isort_radix_sort_host_u32(pin_, pout, n, 0))
+        assert np.array_equal(got(), want), ("radix", n, pinned)
+        _lib.check(lib.isort_bucket_sort_host_u32(pin_, pout, n, U32_MAX, 0))
+        assert np.array_equal(got(), want), ("bucket", n, pinned)
+
+
+def test_host_bucket_entry_reports_range_error(cuda):
+    from paper_1206_3511_b200 import _lib
+
+    lib = _lib.load()
+    keys = np.array([5, 1, 900, 3, 901], dtype=np.uint32)
+    out = np.zeros_like(keys)
+    rc = lib.isort_bucket_sort_host_u32(keys.ctypes.data, out.ctypes.data, keys.size, 899, 0)
+    assert rc != 0
+    assert b"900" in lib.isort_last_error()
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 4, 5, 4096, 4097, 1_000_003])
+def test_is_sorted_u32(cuda, n):
+    """isort_is_sorted_u32 (verify::is_sorted, verify.cpp:67-74): true on sorted
+    and constant input, false with one inversion anywhere (first pair, last pair,
+    a vector boundary), true for n <= 1."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    rng = np.random.default_rng(n)
+    k = np.sort(rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32))
+    t = torch.from_numpy(k.view(np.int32)).cuda()
+    assert device.is_sorted_u32(t) is True
+    assert device.is_sorted_u32(torch.zeros(n, dtype=torch.int32, device="cuda")) is True
+    if n < 2:
+        return
+    for pos in sorted({0, n - 2, min(3, n - 2), min(n // 2, n - 2)}):
+        bad = k.copy()
+        if bad[pos] == 0:
+            bad[pos] = 1
+        bad[pos + 1] = bad[pos] - np.uint32(1)  # one inversion at (pos, pos + 1)
+        assert bad[pos] > bad[pos + 1]
+        tb = torch.from_numpy(bad.view(np.int32)).cuda()
+        assert device.is_sorted_u32(tb) is False, (n, pos)

@@ -4,6 +4,7 @@ Builds tools/libisort_timing.so, sorts 1e8 keys once per digit slot, and reads t
 accumulated clock64 deltas that the instrumented kernel leaves in RadixState.hist
 (the histograms are no longer needed when a pass runs)."""
 import ctypes
+import glob
 import os
 import subprocess
 import sys
@@ -14,8 +15,7 @@ so = os.path.join(ROOT, "tools", "libisort_timing.so")
 if not os.path.exists(so) or "--rebuild" in sys.argv:
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                     "-DISORT_PHASE_TIMING", "-Xcompiler", "-fPIC", "-shared", "-o", so,
-                    os.path.join(ROOT, "paper_1206_3511_b200", "csrc", "isort_api.cu"),
-                    os.path.join(ROOT, "paper_1206_3511_b200", "csrc", "sequence_io.cu")], check=True)
+                    *sorted(glob.glob(os.path.join(ROOT, "paper_1206_3511_b200", "csrc", "*.cu")))], check=True)
 if "--build-only" in sys.argv:
     sys.exit(0)
 import numpy as np
