@@ -147,9 +147,9 @@ enum BucketMode : int { kPow2Narrow = 0, kMagicNarrow = 1, kWide = 2 };
 template <int MODE>
 __device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t key) {
     if (MODE == kWide) return bi.bucket(key);
-    if (MODE == kPow2Narrow) {  // base == 0 (choose_bucket_mode)
-        if (key > bi.bound) return bi.count - 1;
-        return bi.pow2_shift >= 64 ? 0ull : (bi.count * key) >> bi.pow2_shift;
+    if (MODE == kPow2Narrow) {  // n * (key - base) < 2^64 (choose_bucket_mode)
+        if (key - bi.base > bi.span) return key > bi.bound ? bi.count - 1 : 0;
+        return bi.pow2_shift >= 64 ? 0ull : (bi.count * (key - bi.base)) >> bi.pow2_shift;
     }
     const uint64_t k = key - bi.base;
     if (k > bi.span) return key > bi.bound ? bi.count - 1 : 0;  // outside [base, M]: clamped
@@ -164,7 +164,11 @@ __device__ __forceinline__ uint64_t bucket_of(const BucketIndexer& bi, uint64_t 
     return q;
 }
 
+// u32 keys always sort on a power-of-two bucket grid (kPow2Narrow, see
+// BucketDigitizer::make): n < 2^32 and key - base < 2^32 keep n * (key - base)
+// below 2^64 for every range [base, M].
 inline int choose_bucket_mode(uint64_t count, uint64_t bound, uint64_t key_max, uint64_t base = 0) {
+    if (key_max <= 0xFFFFFFFFull) return kPow2Narrow;
     const uint64_t kmax = (bound < key_max ? bound : key_max) - base;
     const bool narrow = static_cast<unsigned __int128>(count) * kmax < (static_cast<unsigned __int128>(1) << 64);
     if (!narrow) return kWide;
@@ -195,9 +199,27 @@ struct BucketDigitizer {
     uint32_t dmask[kBucketMaxDigits];
     uint32_t check_range;              // [base, M] narrower than the key type: keys can be out of range
 
+    // The pipeline may group keys by ANY bucket function that is monotone in the
+    // key: the final segment sort makes the output the unique stable sort by key
+    // either way.  kPow2Narrow therefore rounds the range
+    // [base, M] up to a power-of-two span 2^s and uses b = (n * (key - base)) >> s
+    // -- one multiply and a shift for every bound M, against a 64-bit reciprocal
+    // for the reference's exact floor(n * key / (M + 1)) (which only changes how
+    // evenly the n buckets are filled: at most 2x fewer of them are used).  The
+    // range check keeps the exact [base, M].  The exact reference bucket_index is
+    // BucketIndexer::bucket (isort_bucket_index_u64, pinned by tests).
     static BucketDigitizer make(uint64_t n, uint64_t bound, uint64_t base = 0) {
         BucketDigitizer d{};
-        d.bi = BucketIndexer::make(n, bound, base);
+        uint64_t grid = bound;  // inclusive upper end of the bucket grid
+        if (MODE == kPow2Narrow) {  // the grid need not reach past the key type's maximum
+            const uint64_t kmax = static_cast<uint64_t>(static_cast<K>(~static_cast<K>(0)));
+            const uint64_t span = (bound < kmax ? bound : kmax) - (base < kmax ? base : kmax);
+            const uint32_t s = span ? 64 - __builtin_clzll(span) : 0;  // 2^s > span
+            grid = s >= 64 ? ~0ull : base + ((1ull << s) - 1);
+        }
+        d.bi = BucketIndexer::make(n, grid, base);
+        d.bi.bound = bound;  // exact range: clamping and the range check
+        d.bi.span = bound - base;
         const uint32_t L = n > 1 ? 64 - __builtin_clzll(n - 1) : 0;  // bits of the largest bucket index
         uint32_t db = L > kSuperBucketBits ? (L - kSuperBucketBits + 7) / 8 : 0;
         if (db > kBucketMaxDigits) db = kBucketMaxDigits;
@@ -239,8 +261,9 @@ struct BucketDigitizer {
     // Digit of the bucket index.  Keys outside [base, M] only reach here when the
     // call is failing with a range error; their digits are then meaningless but < 256.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
-        if (MODE == kPow2Narrow) {  // floor(n * key / 2^s) >> shift = (n * key) >> (s + shift); n < 2^32
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+        if (MODE == kPow2Narrow) {  // floor(n * k / 2^s) >> shift = (n * k) >> (s + shift); n, k < 2^32
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) *
+                               (static_cast<uint64_t>(key) - bi.base);
             return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
         }
         return static_cast<uint32_t>(bidx(key) >> sh) & (kRadix - 1);
@@ -248,7 +271,8 @@ struct BucketDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         if (MODE == kPow2Narrow) {
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * static_cast<uint64_t>(key);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) *
+                               (static_cast<uint64_t>(key) - bi.base);
 #pragma unroll
             for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;
@@ -258,7 +282,6 @@ struct BucketDigitizer {
         for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(b >> shift[q]) & (kRadix - 1);
     }
     __device__ __forceinline__ bool in_range(K key) const {
-        if (MODE == kPow2Narrow) return !check_range || static_cast<uint64_t>(key) <= bi.bound;  // base 0
         return !check_range || static_cast<uint64_t>(key) - bi.base <= bi.span;
     }
     __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }

@@ -700,16 +700,21 @@ int bucket_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vou
     if (base > bound)
         return set_error(ISORT_EINVAL, "isort_bucket_sort: range base %llu above range bound %llu",
                          (unsigned long long)base, (unsigned long long)bound);
-    switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)), base)) {
-        case kPow2Narrow:
-            return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                                    async_status, base);
-        case kMagicNarrow:
-            return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                                     async_status, base);
-        default:
-            return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
-                                              async_status, base);
+    if constexpr (sizeof(K) == 4) {  // u32 keys: always the power-of-two grid (choose_bucket_mode)
+        return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                async_status, base);
+    } else {
+        switch (choose_bucket_mode(n, bound, static_cast<uint64_t>(~static_cast<K>(0)), base)) {
+            case kPow2Narrow:
+                return bucket_sort_impl<K, kPow2Narrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                        async_status, base);
+            case kMagicNarrow:
+                return bucket_sort_impl<K, kMagicNarrow>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                         async_status, base);
+            default:
+                return bucket_sort_impl<K, kWide>(kin, kout, vin, vout, n, bound, vmode, temp, temp_bytes, s,
+                                                  async_status, base);
+        }
     }
 }
 
