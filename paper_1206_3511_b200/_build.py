@@ -14,6 +14,7 @@ import os
 import shutil
 import subprocess
 import sys
+import time
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -63,8 +64,10 @@ def build_engine(force: bool = False, verbose: bool = False, jobs: int | None = 
         cmd = [_nvcc(), *NVCC_FLAGS, "-c", "-o", o + ".tmp", u]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
+        t0 = time.time()
         subprocess.run(cmd, check=True, cwd=CSRC)
         os.replace(o + ".tmp", o)
+        os.utime(o, (t0, t0))  # a source edited while this unit compiled still counts as newer
 
     if todo:
         with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:

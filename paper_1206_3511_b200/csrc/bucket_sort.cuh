@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
     constexpr int kStage = BLOCK * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    if (rst->descents == 0 || rst->reversed || rst->first_bad != 0) return;  // sorted / reversed / range error
+    if (rst->descents == 0 || rst->reversed || rst->counting || rst->first_bad != 0)
+        return;  // sorted / reversed / counting pass / range error
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();

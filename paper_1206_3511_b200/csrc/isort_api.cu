@@ -172,6 +172,7 @@ RadixLayout radix_layout(uint64_t n, bool vals) {
     size_t off = 0;
     L.state = off;
     off += align_up(sizeof(RadixState));
+    off += align_up(sizeof(CountState));  // count_state(): zeroed with the state
     L.lookback = off;
     off += align_up(static_cast<size_t>(KeyTraits<K>::kDigits) * lb_tiles * kRadix * lb_word_bytes(n));
     L.keys_alt = off;
@@ -240,7 +241,7 @@ int radix_sort_device(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout
         return launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, vmode == ISORT_VALS_IOTA, n, st, lb,
                                               L.tiles, dz, true, true, s);
     return launch_radix_pipeline<K, false>(kin, kout, kalt, nullptr, nullptr, nullptr, false, n, st, lb, L.tiles, dz,
-                                           true, true, s);
+                                           kPlanSkipSorted | kPlanCounting, true, s);
 }
 
 // ------------------------------------------------------- host-side helpers
@@ -745,10 +746,14 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
     const BucketDigitizer<K, MODE> dz = BucketDigitizer<K, MODE>::make(n, bound, base);
     const bool iota = vmode == ISORT_VALS_IOTA;
 
+    // M < kCountBins <= n: every bucket holds one key value, so a keys-only bucket
+    // sort is the counting pass (K6) -- bucket b's contents are cnt copies of its value
+    const int flags = kPlanSkipSorted | (base == 0 && bound < static_cast<uint64_t>(kCountBins) && n > bound
+                                             ? kPlanCounting : 0);
     int rc = vals ? launch_radix_pipeline<K, true>(kin, kout, kalt, vin, vout, valt, iota, n, st, lb, L.r.tiles, dz,
-                                                   true, true, s)
+                                                   flags, true, s)
                   : launch_radix_pipeline<K, false>(kin, kout, kalt, nullptr, nullptr, nullptr, false, n, st, lb,
-                                                    L.r.tiles, dz, true, true, s);
+                                                    L.r.tiles, dz, flags, true, s);
     if (rc) return rc;
     ISORT_CUDA_TRY(cudaMemsetAsync(bst, 0, sizeof(BucketState), s));
     const int rank_ok = rank_state();

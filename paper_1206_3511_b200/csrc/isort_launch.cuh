@@ -93,6 +93,12 @@ struct UpfrontCfg {
 
 constexpr int kUpfrontBlock = ISORT_UF_BLOCK;
 
+// The counting pass's state sits right after RadixState in every temp layout
+// (radix_layout), inside the region the pipeline zeroes.
+inline CountState* count_state(RadixState* st) {
+    return reinterpret_cast<CountState*>(reinterpret_cast<char*>(st) + align_up(sizeof(RadixState)));
+}
+
 // Bytes per look-back status word for a call over n keys (radix_onesweep.cuh).
 inline size_t lb_word_bytes(uint64_t n) { return n <= kNarrowLbMaxN ? 4 : 8; }
 
@@ -124,7 +130,7 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, u
 template <typename K, bool VALS, typename Dz>
 int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
                           uint32_t* valt, bool iota, uint64_t n, RadixState* st, void* lookback,
-                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
+                          uint32_t tiles, const Dz& dz, int plan_flags, bool zero_state,
                           cudaStream_t s);
 template <typename K, typename Dz, bool VALS>
 void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, BucketState* bst, const Dz& dz,
@@ -193,10 +199,11 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, u
 template <typename K, bool VALS, typename Dz>
 int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout,
                           uint32_t* valt, bool iota, uint64_t n, RadixState* st, void* lookback,
-                          uint32_t tiles, const Dz& dz, bool skip_sorted, bool zero_state,
+                          uint32_t tiles, const Dz& dz, int plan_flags, bool zero_state,
                           cudaStream_t s) {
     constexpr int D = Dz::kDigits;
-    int rc = launch_histogram<K, Dz>(kin, n, st, lookback, tiles, dz, skip_sorted ? kPlanSkipSorted : 0, zero_state, s);
+    if (VALS) plan_flags &= ~kPlanCounting;  // a payload needs the scatter
+    int rc = launch_histogram<K, Dz>(kin, n, st, lookback, tiles, dz, plan_flags, zero_state, s);
     if (rc) return rc;
 
     if (n < kSmallN)
@@ -215,15 +222,28 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
         k_reverse_keys<K><<<cgrid, 512, 0, s>>>(kin, kout, n, st);
         launched(2);
     } else {
-        auto* head = static_cast<long long*>(lookback);  // the look-back rows are unused on this path
-        auto* end = head + (n + kRevTile - 1) / kRevTile;
+        // the look-back rows are unused on this path: they hold the long-run list
+        // (at most n / (kRevShortRun + 1) runs of 16 bytes, well inside the rows)
+        auto* long_runs = static_cast<unsigned long long*>(lookback);
         const unsigned rgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
-        k_rev_tile_bounds<K><<<rgrid, kRevBlock, 0, s>>>(kin, n, st, head, end);
-        k_rev_carry<<<1, 1024, 0, s>>>(n, st, head, end);
-        k_rev_scatter<K, true><<<rgrid, kRevBlock, 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st, head, end);
-        launched(4);
+        k_reverse_pairs<K><<<cgrid, 512, 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st);
+        k_rev_fix_runs<K><<<cgrid, 512, 0, s>>>(kout, vout, n, st, long_runs);
+        k_rev_long_runs<<<rgrid, 512, 0, s>>>(vout, st, long_runs);
+        launched(3);
     }
     prof_mark(s, "reverse");
+    if (plan_flags & kPlanCounting) {  // small key range (K6): counts + fill, if the plan chose it
+        CountState* cs = count_state(st);
+        constexpr size_t kHistSmem = static_cast<size_t>(kCountBins) * kCountRep * sizeof(uint32_t);
+        auto* kh = k_count_hist<K>;
+        set_max_smem_once(kh, kHistSmem);
+        const unsigned hgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
+        kh<<<hgrid, kCountBlock, kHistSmem, s>>>(kin, n, st, cs);
+        prof_mark(s, "count_hist");
+        k_count_fill<K><<<hgrid, kCountBlock, 0, s>>>(kout, n, st, cs);
+        prof_mark(s, "count_fill");
+        launched(2);
+    }
     ISORT_CUDA_TRY(cudaGetLastError());
     return ISORT_OK;
 }
@@ -246,7 +266,7 @@ void launch_segments(K* keys, uint32_t* vals, uint64_t n, const RadixState* st, 
 // Explicit instantiation helpers for the inst_*.cu units.
 #define ISORT_INST_PIPELINE(K, V, DZ)                                                                       \
     template int launch_radix_pipeline<K, V, DZ>(const K*, K*, K*, const uint32_t*, uint32_t*, uint32_t*, bool, \
-                                                 uint64_t, RadixState*, void*, uint32_t, const DZ&, bool, bool,  \
+                                                 uint64_t, RadixState*, void*, uint32_t, const DZ&, int, bool,   \
                                                  cudaStream_t);
 #define ISORT_INST_HISTOGRAM(K, DZ) \
     template int launch_histogram<K, DZ>(const K*, uint64_t, RadixState*, void*, uint32_t, const DZ&, int, bool, cudaStream_t);

@@ -55,11 +55,19 @@ struct RadixState {
     uint32_t n_active;                  // K2
     uint32_t copy_in_to_out;            // K2: sorted input, out = in
     uint32_t reversed;                  // K2: non-increasing input, out = in reversed run by run
+    uint32_t counting;                  // K2: keys-only, max < kCountBins: one counting pass (K6)
+    uint32_t rev_long;                  // K5: runs longer than kRevShortRun listed for k_rev_long_runs
     uint32_t tile_ticket[kMaxDigits];   // K3
     int32_t digit_of_slot[kMaxDigits];  // K2
     int32_t src_of_slot[kMaxDigits];
     int32_t dst_of_slot[kMaxDigits];
     unsigned long long prof[16];        // debug counters (ISORT_PHASE_TIMING builds)
+};
+// Keys-only sorts whose largest key is below kCountBins take one counting pass
+// on the whole key (a single kCountBits-bit digit) instead of digit passes; see K6.
+constexpr int kCountBits = 12, kCountBins = 1 << kCountBits;
+struct CountState {
+    uint32_t vhist[kCountBins];  // K6a: occurrences of each key value
 };
 
 // ------------------------------------------------------------- digitizers
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
 // One CTA of kRadix threads.  flags: kPlanSkipSorted (a sorted input needs no
 // pass), kPlanKeepTrivial (run every digit pass, even one-digit ones: a scatter
 // pass must move the keys).
-constexpr int kPlanSkipSorted = 1, kPlanKeepTrivial = 2;
+constexpr int kPlanSkipSorted = 1, kPlanKeepTrivial = 2, kPlanCounting = 4;
 template <int D>
 __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, uint64_t n, int flags) {
     __shared__ uint32_t warp_tot[kRadix / 32];
@@ -261,16 +269,22 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
         // equal keys kept in input order (k_reverse_runs), no digit pass
         const bool reversed = (flags & kPlanSkipSorted) && !sorted && st->ascents == 0;
         const bool keep = (flags & kPlanKeepTrivial) != 0;
+        // keys only and every key below kCountBins: the LSD sort is one pass on a
+        // kCountBits-bit digit (the whole key), and a stable pass over keys that
+        // carry nothing else is determined by the key counts alone (K6)
+        const bool counting = (flags & kPlanCounting) && !sorted && !reversed && !keep &&
+                              st->max_key < static_cast<unsigned long long>(kCountBins);
         int na = 0;
         for (int p = 0; p < D; ++p)
-            if (keep || (!sorted && !reversed && !trivial[p])) st->digit_of_slot[na++] = p;
+            if (keep || (!sorted && !reversed && !counting && !trivial[p])) st->digit_of_slot[na++] = p;
         for (int s = 0; s < na; ++s) {
             st->src_of_slot[s] = s == 0 ? kBufIn : st->dst_of_slot[s - 1];
             st->dst_of_slot[s] = ((na - 1 - s) % 2 == 0) ? kBufOut : kBufAlt;
         }
         st->n_active = na;
-        st->copy_in_to_out = na == 0 && !reversed;
+        st->copy_in_to_out = na == 0 && !reversed && !counting;
         st->reversed = reversed;
+        st->counting = counting;
     }
 }
 
@@ -901,153 +915,256 @@ __global__ void k_copy_if_unsorted_skip(const K* __restrict__ in, K* __restrict_
 }
 
 
+// ------------------------------------------------------------------- K6
+// Counting pass (keys only, every key < kCountBins): the LSD sort with one
+// kCountBits-bit digit = the whole key.  A stable counting pass places key v at
+// offs[v] + (its arrival rank among the v's) (sort.cpp:95-108); with nothing but
+// the key to carry, those slots are exactly the run [offs[v], offs[v] + cnt[v])
+// filled with v, so the pass needs the counts (K6a: 4n B read) and a fill of the
+// output (K6b: 4n B write) -- no scatter.  Both return at once unless the plan
+// chose this path (no host round trip; graph-capturable).
+constexpr int kCountBlock = 1024;
+constexpr int kCountRep = 4;  // counter copies per bin (lane % kCountRep): fewer same-address lanes
+
+template <typename K>
+__global__ void __launch_bounds__(kCountBlock) k_count_hist(const K* __restrict__ keys, uint64_t n,
+                                                            const RadixState* __restrict__ st,
+                                                            CountState* __restrict__ cs) {
+    if (!st->counting) return;
+    extern __shared__ __align__(16) uint32_t ch[];  // kCountBins * kCountRep
+    for (int i = threadIdx.x; i < kCountBins * kCountRep; i += kCountBlock) ch[i] = 0;
+    __syncthreads();
+    uint32_t* my = ch + (lane_id() % kCountRep);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kCountBlock;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kCountBlock + threadIdx.x;
+    uint64_t done = 0;
+    if (sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(keys) & 15u) == 0) {
+        const uint64_t nv = n / 4;
+        const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+        for (uint64_t v = t0; v < nv; v += stride) {
+            const uint4 q = ldg_stream_v4(k4 + v);
+            atomicAdd(my + q.x * kCountRep, 1u);
+            atomicAdd(my + q.y * kCountRep, 1u);
+            atomicAdd(my + q.z * kCountRep, 1u);
+            atomicAdd(my + q.w * kCountRep, 1u);
+        }
+        done = nv * 4;
+    }
+    for (uint64_t i = done + t0; i < n; i += stride) atomicAdd(my + static_cast<uint32_t>(keys[i]) * kCountRep, 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kCountBins; b += kCountBlock) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int r = 0; r < kCountRep; ++r) c += ch[b * kCountRep + r];
+        if (c) atomicAdd(&cs->vhist[b], c);
+    }
+}
+
+// Every CTA scans the kCountBins counts into shared memory (16 KB from L2), then
+// writes its share of the output in 16-byte vectors: position p holds the v with
+// offs[v] <= p < offs[v + 1] (a binary search per vector, then a walk).
+template <typename K>
+__global__ void __launch_bounds__(kCountBlock, 2) k_count_fill(K* __restrict__ out, uint64_t n,
+                                                            const RadixState* __restrict__ st,
+                                                            const CountState* __restrict__ cs) {
+    if (!st->counting) return;
+    __shared__ uint32_t ends[kCountBins];  // inclusive prefix: ends[v] = offs[v] + cnt[v]
+    __shared__ uint32_t wtot[kCountBlock / 32];
+    constexpr int kPer = kCountBins / kCountBlock;
+    uint32_t c[kPer], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        c[j] = cs->vhist[threadIdx.x * kPer + j];
+        sum += c[j];
+    }
+    const uint32_t inc = warp_inclusive_scan(sum);
+    if (lane_id() == 31) wtot[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    uint32_t run = inc - sum;
+    for (int w = 0; w < static_cast<int>(threadIdx.x >> 5); ++w) run += wtot[w];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        run += c[j];
+        ends[threadIdx.x * kPer + j] = run;
+    }
+    __syncthreads();
+    auto value_at = [&](uint32_t p, uint32_t hint) -> uint32_t {  // smallest v with ends[v] > p, v >= hint
+        while (ends[hint] <= p) ++hint;
+        return hint;
+    };
+    auto search = [&](uint32_t p) -> uint32_t {  // smallest v with ends[v] > p
+        uint32_t lo = 0, hi = kCountBins - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ends[mid] > p) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    constexpr uint32_t E = 16 / sizeof(K);
+    constexpr int U = 4;  // vectors per lane per warp step (32 * U * E positions)
+    const uint64_t nv = (reinterpret_cast<uintptr_t>(out) & 15u) == 0 ? n / E : 0;
+    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (kCountBlock / 32) * 32 * U;
+    // warp-converged loop: one broadcast binary search for the warp step's first
+    // position, then every vector walks forward from it (a step per distinct value)
+    for (uint64_t vb = (static_cast<uint64_t>(blockIdx.x) * (kCountBlock / 32) + (threadIdx.x >> 5)) * 32 * U;
+         vb < nv; vb += wstride) {
+        const uint32_t w0 = search(static_cast<uint32_t>(vb * E));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t v = vb + u * 32 + lane_id();
+            if (v >= nv) break;
+            const uint32_t p = static_cast<uint32_t>(v * E);
+            uint32_t x[E];
+            x[0] = value_at(p, w0);
+#pragma unroll
+            for (uint32_t j = 1; j < E; ++j) x[j] = value_at(p + j, x[j - 1]);
+            // values < 2^12: a u64 key is (value, 0)
+            reinterpret_cast<uint4*>(out)[v] = sizeof(K) == 4 ? make_uint4(x[0], x[1 % E], x[2 % E], x[3 % E])
+                                                              : make_uint4(x[0], 0u, x[1 % E], 0u);
+        }
+    }
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kCountBlock;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kCountBlock + threadIdx.x;
+    for (uint64_t i = nv * E + t0; i < n; i += stride) out[i] = static_cast<K>(search(static_cast<uint32_t>(i)));
+}
+
 // ------------------------------------------------------------------- K5
 // Non-increasing input (K1: no ascent): the stable sort is the reversal in
-// which every run of equal keys keeps its input order.  A run [a, b) of the
-// input lands at [n - b, n - a), so element i goes to n - b(i) + (i - a(i)).
+// which every run of equal keys keeps its input order.
 // Keys only: equal keys are indistinguishable, so out[n - 1 - i] = in[i] is
-// already exact (one read, one write, like the sorted-input copy).  With a
-// payload the run bounds matter: per 4096-key tile, k_rev_tile_bounds records
-// the last run start and the first run end in the tile, k_rev_carry scans
-// them across tiles (prefix max / suffix min), and k_rev_scatter finishes a(i)
-// and b(i) with block scans and moves keys and payload.  Every kernel returns at
-// once unless the plan chose this path (no host round trip; graph-capturable).
-constexpr int kRevTile = 4096, kRevBlock = 512, kRevPer = kRevTile / kRevBlock;
+// already exact (one read, one write, like the sorted-input copy).
+// With a payload: the same full reversal of keys and payload (coalesced: a
+// warp's stores land on consecutive descending addresses), then every run of
+// equal keys in the output gets its payload reversed back into input order.
+// k_rev_fix_runs finds the runs (a run's first thread sees key[i-1] != key[i] ==
+// key[i+1]) and finds its end by a galloping search on the sorted output; runs up
+// to kRevShortRun keys are reversed by that thread, longer ones are listed for
+// k_rev_long_runs (one CTA per run).  Every kernel returns at once unless the
+// plan chose this path (no host round trip; graph-capturable).
+constexpr int kRevShortRun = 64;
+
+// 16-byte vectors reversed as whole vectors when n is a multiple of the vector
+// width (in[4v..4v+3] -> out[n-4-4v..]: both sides aligned), scalar otherwise.
+template <typename K>
+__device__ __forceinline__ uint4 reverse_vec(uint4 q) {
+    return sizeof(K) == 4 ? make_uint4(q.w, q.z, q.y, q.x) : make_uint4(q.z, q.w, q.x, q.y);
+}
 
 template <typename K>
 __global__ void k_reverse_keys(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
                                const RadixState* __restrict__ st) {
     if (!st->reversed) return;
+    constexpr uint64_t E = 16 / sizeof(K);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        out[n - 1 - i] = in[i];
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (n % E == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) {
+        const uint64_t nv = n / E;
+        for (uint64_t v = t0; v < nv; v += stride)
+            reinterpret_cast<uint4*>(out)[nv - 1 - v] = reverse_vec<K>(ldg_stream_v4(reinterpret_cast<const uint4*>(in) + v));
+        return;
+    }
+    for (uint64_t i = t0; i < n; i += stride) out[n - 1 - i] = in[i];
 }
 
-// run start / run end flags of position i (K >= 2 elements compared as keys)
 template <typename K>
-__device__ __forceinline__ bool rev_head(const K* keys, uint64_t i) { return i == 0 || keys[i - 1] != keys[i]; }
-template <typename K>
-__device__ __forceinline__ bool rev_end(const K* keys, uint64_t i, uint64_t n) {
-    return i + 1 == n || keys[i] != keys[i + 1];
-}
-
-// Per tile: the last run start in the tile (or -1) and the first run end (exclusive
-// index; INT64_MAX when no run ends in the tile).
-template <typename K>
-__global__ void __launch_bounds__(kRevBlock) k_rev_tile_bounds(const K* __restrict__ keys, uint64_t n,
-                                                              const RadixState* __restrict__ st,
-                                                              long long* __restrict__ last_head,
-                                                              long long* __restrict__ first_end) {
+__global__ void k_reverse_pairs(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
+                                uint32_t* __restrict__ vout, int iota_vals, uint64_t n,
+                                const RadixState* __restrict__ st) {
     if (!st->reversed) return;
-    const uint64_t tiles = (n + kRevTile - 1) / kRevTile;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        long long h = -1, e = LLONG_MAX;
-        for (int j = 0; j < kRevPer; ++j) {
-            const uint64_t i = t * kRevTile + static_cast<uint64_t>(j) * kRevBlock + threadIdx.x;
-            if (i < n) {
-                if (rev_head(keys, i)) h = max(h, static_cast<long long>(i));
-                if (rev_end(keys, i, n)) e = min(e, static_cast<long long>(i) + 1);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(kout) |
+                           reinterpret_cast<uintptr_t>(vin) | reinterpret_cast<uintptr_t>(vout)) & 15u) == 0;
+    if (sizeof(K) == 4 && n % 4 == 0 && aligned) {  // 4 keys + 4 payload words per thread step
+        const uint64_t nv = n / 4;
+        for (uint64_t v = t0; v < nv; v += stride) {
+            reinterpret_cast<uint4*>(kout)[nv - 1 - v] = reverse_vec<K>(ldg_stream_v4(reinterpret_cast<const uint4*>(kin) + v));
+            const uint32_t b = static_cast<uint32_t>(4 * v);
+            const uint4 q = iota_vals ? make_uint4(b, b + 1, b + 2, b + 3) : ldg_stream_v4(reinterpret_cast<const uint4*>(vin) + v);
+            reinterpret_cast<uint4*>(vout)[nv - 1 - v] = make_uint4(q.w, q.z, q.y, q.x);
+        }
+        return;
+    }
+    for (uint64_t i = t0; i < n; i += stride) {
+        kout[n - 1 - i] = kin[i];
+        vout[n - 1 - i] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
+    }
+}
+
+// End of the run of key k that starts at i in the ascending array `keys`.
+template <typename K>
+__device__ __forceinline__ uint64_t run_end(const K* __restrict__ keys, uint64_t n, uint64_t i, K k) {
+    uint64_t lo = i + 1, step = 1;  // keys[lo - 1] == k
+    uint64_t hi = lo;
+    while (hi < n && keys[hi] == k) {  // gallop: keys[hi] == k  =>  the end is past hi
+        lo = hi + 1;
+        hi = lo + step < n ? lo + step : n;
+        step <<= 1;
+    }
+    while (lo < hi) {  // first index in [lo, hi) with keys[idx] != k
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (keys[mid] == k) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename K>
+__global__ void k_rev_fix_runs(const K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
+                               RadixState* __restrict__ st, unsigned long long* __restrict__ long_runs) {
+    if (!st->reversed) return;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const bool vec = sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(keys) & 15u) == 0;
+    // a thread checks positions [4g, 4g + 4) per step: one 16-byte load of them plus
+    // the keys just before and after (L1 hits); a run that ends inside that window
+    // needs no further load
+    const uint64_t groups = (n + 3) / 4;
+    for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        const uint64_t b0 = 4 * g;
+        K w[6];  // keys[b0 - 1 .. b0 + 4]; positions >= n never match (checked by index)
+        if (vec && b0 + 4 <= n) {
+            const uint4 q = ldg_stream_v4(reinterpret_cast<const uint4*>(keys) + g);
+            w[1] = static_cast<K>(q.x), w[2] = static_cast<K>(q.y), w[3] = static_cast<K>(q.z), w[4] = static_cast<K>(q.w);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[1 + j] = b0 + j < n ? keys[b0 + j] : static_cast<K>(0);
+        }
+        w[0] = b0 > 0 ? keys[b0 - 1] : static_cast<K>(0);
+        w[5] = b0 + 4 < n ? keys[b0 + 4] : static_cast<K>(0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t i = b0 + j;
+            const K k = w[1 + j];
+            if (!(i + 1 < n && w[2 + j] == k && (i == 0 || w[j] != k))) continue;  // no run of >= 2 starts at i
+            uint64_t e = i + 2;  // first position past the run, within the window if possible
+#pragma unroll
+            for (int t = 3 + j; t <= 5; ++t)
+                if (e == b0 + t - 1 && e < n && w[t] == k) ++e;
+            if (e == b0 + 5 && e < n) e = run_end(keys, n, i, k);  // the run leaves the window
+            if (e - i > static_cast<uint64_t>(kRevShortRun)) {
+                const uint32_t slot = atomicAdd(&st->rev_long, 1u);
+                long_runs[2 * slot] = i;
+                long_runs[2 * slot + 1] = e;
+                continue;
+            }
+            for (uint64_t a = i, b = e - 1; a < b; ++a, --b) {
+                const uint32_t t = vals[a];
+                vals[a] = vals[b];
+                vals[b] = t;
             }
         }
-        h = block_reduce_max_ll<kRevBlock>(h);
-        e = -block_reduce_max_ll<kRevBlock>(-e);
-        if (threadIdx.x == 0) {
-            last_head[t] = h;
-            first_end[t] = e;
-        }
     }
 }
 
-// One CTA: carry_head[t] = max(last_head[0..t-1]) and carry_end[t] =
-// min(first_end[t+1..]) in place of the inputs.
-static __global__ void __launch_bounds__(1024) k_rev_carry(uint64_t n, const RadixState* __restrict__ st,
-                                                    long long* __restrict__ head, long long* __restrict__ end) {
+static __global__ void k_rev_long_runs(uint32_t* __restrict__ vals, const RadixState* __restrict__ st,
+                                const unsigned long long* __restrict__ long_runs) {
     if (!st->reversed) return;
-    const long long tiles = static_cast<long long>((n + kRevTile - 1) / kRevTile);
-    const long long per = (tiles + 1023) / 1024;
-    const long long lo = threadIdx.x * per, hi = min(tiles, lo + per);
-    long long hm = -1, em = LLONG_MAX;
-    for (long long t = lo; t < hi; ++t) hm = max(hm, head[t]);
-    for (long long t = lo; t < hi; ++t) em = min(em, end[t]);
-    __shared__ long long sh[1024], se[1024];
-    sh[threadIdx.x] = hm;
-    se[threadIdx.x] = em;
-    __syncthreads();
-    long long ph = -1, pe = LLONG_MAX;  // exclusive prefix max over threads < me / suffix min over threads > me
-    for (int k = 0; k < static_cast<int>(threadIdx.x); ++k) ph = max(ph, sh[k]);
-    for (int k = threadIdx.x + 1; k < 1024; ++k) pe = min(pe, se[k]);
-    __syncthreads();
-    for (long long t = lo; t < hi; ++t) {  // forward: exclusive prefix max
-        const long long v = head[t];
-        head[t] = ph;
-        ph = max(ph, v);
-    }
-    for (long long t = hi - 1; t >= lo; --t) {  // backward: exclusive suffix min
-        const long long v = end[t];
-        end[t] = pe;
-        pe = min(pe, v);
-    }
-}
-
-template <typename K, bool VALS>
-__global__ void __launch_bounds__(kRevBlock) k_rev_scatter(const K* __restrict__ kin, K* __restrict__ kout,
-                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
-                                                          int iota_vals, uint64_t n, const RadixState* __restrict__ st,
-                                                          const long long* __restrict__ carry_head,
-                                                          const long long* __restrict__ carry_end) {
-    if (!st->reversed) return;
-    __shared__ long long s_h[kRevBlock / 32], s_e[kRevBlock / 32];
-    const uint64_t tiles = (n + kRevTile - 1) / kRevTile;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        // thread owns positions [base, base + kRevPer) of the tile (blocked)
-        const uint64_t base = t * kRevTile + static_cast<uint64_t>(threadIdx.x) * kRevPer;
-        long long a[kRevPer], b[kRevPer];
-        long long run = -1;
-#pragma unroll
-        for (int j = 0; j < kRevPer; ++j) {
-            const uint64_t i = base + j;
-            if (i < n && rev_head(kin, i)) run = static_cast<long long>(i);
-            a[j] = run;  // -1: the run started before this thread's positions
-        }
-        long long eend = LLONG_MAX;
-#pragma unroll
-        for (int j = kRevPer - 1; j >= 0; --j) {
-            const uint64_t i = base + j;
-            if (i < n && rev_end(kin, i, n)) eend = static_cast<long long>(i) + 1;
-            b[j] = eend;  // LLONG_MAX: the run ends after this thread's positions
-        }
-        // block exclusive prefix max of the threads' last heads, suffix min of first ends
-        long long inc_h = a[kRevPer - 1], inc_e = b[0];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long th = __shfl_up_sync(ISORT_FULL_MASK, inc_h, o);
-            const long long te = __shfl_down_sync(ISORT_FULL_MASK, inc_e, o);
-            if (lane >= static_cast<uint32_t>(o)) inc_h = max(inc_h, th);
-            if (lane + o < 32) inc_e = min(inc_e, te);
-        }
-        __syncthreads();
-        if (lane == 31) s_h[warp] = inc_h;
-        if (lane == 0) s_e[warp] = inc_e;
-        __syncthreads();
-        long long ex_h = __shfl_up_sync(ISORT_FULL_MASK, inc_h, 1);
-        long long ex_e = __shfl_down_sync(ISORT_FULL_MASK, inc_e, 1);
-        if (lane == 0) ex_h = -1;
-        if (lane == 31) ex_e = LLONG_MAX;
-        for (uint32_t w = 0; w < warp; ++w) ex_h = max(ex_h, s_h[w]);
-        for (uint32_t w = warp + 1; w < kRevBlock / 32; ++w) ex_e = min(ex_e, s_e[w]);
-        ex_h = max(ex_h, carry_head[t]);
-        ex_e = min(ex_e, carry_end[t]);
-#pragma unroll
-        for (int j = 0; j < kRevPer; ++j) {
-            const uint64_t i = base + j;
-            if (i < n) {
-                const long long aa = a[j] >= 0 ? a[j] : ex_h;
-                const long long bb = b[j] != LLONG_MAX ? b[j] : ex_e;
-                const uint64_t p = n - static_cast<uint64_t>(bb) + (i - static_cast<uint64_t>(aa));
-                kout[p] = kin[i];
-                if (VALS) vout[p] = iota_vals ? static_cast<uint32_t>(i) : vin[i];
-            }
+    const uint32_t runs = st->rev_long;
+    for (uint32_t r = blockIdx.x; r < runs; r += gridDim.x) {
+        const uint64_t a = long_runs[2 * r], e = long_runs[2 * r + 1], half = (e - a) / 2;
+        for (uint64_t j = threadIdx.x; j < half; j += blockDim.x) {
+            const uint32_t t = vals[a + j];
+            vals[a + j] = vals[e - 1 - j];
+            vals[e - 1 - j] = t;
         }
     }
 }

@@ -553,6 +553,9 @@ def test_reverse_sorted_early_out_is_stable(cuda, oracle, n):
         "short_runs": np.sort(rng.integers(0, max(2, n // 3), size=n, dtype=np.uint64).astype(np.uint32))[::-1],
         "long_runs": np.sort(rng.integers(0, 5, size=n, dtype=np.uint64).astype(np.uint32))[::-1],
         "constant": np.full(n, 7, dtype=np.uint32),
+        # runs around the short/long fix-up boundary (kRevShortRun = 64)
+        "run_lengths": np.repeat(np.arange(20_000, 0, -1, dtype=np.uint32),
+                                 np.resize([1, 2, 63, 64, 65, 66, 127, 128, 129, 3, 5000], 20_000))[:n],
     }
     for name, k in cases.items():
         k = np.ascontiguousarray(k)
@@ -662,3 +665,45 @@ def test_is_sorted_u32(cuda, n):
         assert bad[pos] > bad[pos + 1]
         tb = torch.from_numpy(bad.view(np.int32)).cuda()
         assert device.is_sorted_u32(tb) is False, (n, pos)
+
+
+# ------------------------------------------------------- small key range: the counting pass (K6)
+@pytest.mark.parametrize("n", [1, 2, 5, 4097, 100_003, 3_000_001])
+@pytest.mark.parametrize("top", [2, 1023, 4095, 4096])
+def test_counting_pass_small_range(cuda, oracle, n, top):
+    """Keys-only sorts with every key < 2^12 take one counting pass (histogram +
+    fill) -- radix always, bucket when M < 2^12 <= n (one value per bucket).
+    max = 4096 must take the digit passes.  Bit-exact against the oracle; with a
+    payload the same inputs take the stable scatter."""
+    rng = np.random.default_rng(n * 7 + top)
+    k = rng.integers(0, top + 1, size=n, dtype=np.uint64).astype(np.uint32)
+    if n >= 2:
+        k[rng.integers(0, n)] = top  # the maximum is present
+    want_k, want_i = oracle.sort_u32(k, with_index=True)
+    got_k, _ = dev_sort(k, "radix", None)
+    assert np.array_equal(got_k, want_k)
+    for bound in (top, max(top, 4095), U32_MAX):
+        got_k, _ = dev_sort(k, "bucket", None, range_bound=bound)
+        assert np.array_equal(got_k, want_k), bound
+    got_k, got_i = dev_sort(k, "radix", "iota")
+    assert np.array_equal(got_k, want_k) and np.array_equal(got_i, want_i)
+
+
+def test_counting_pass_graph_replay_and_reuse(cuda, oracle):
+    """The counting path inside a captured graph, alternating with a wide-range
+    input on the same Sorter (the plan is decided on the device every call)."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    n = 1_000_003
+    small = oracle.uniform_u32(n, 3) & np.uint32(1023)
+    wide = oracle.uniform_u32(n, 4)
+    s = device.Sorter(n, 4, "radix", None, graph=True)
+    ts = torch.from_numpy(small.view(np.int32)).cuda()
+    tw = torch.from_numpy(wide.view(np.int32)).cuda()
+    for _ in range(3):
+        for t, k in ((ts, small), (tw, wide)):
+            got, _ = s(t)
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), np.sort(k))
