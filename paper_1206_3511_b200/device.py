@@ -98,7 +98,8 @@ class Sorter:
             if self._graph is not None and self._graph_key == key:
                 if self._status is not None:
                     self._status.zero_()
-                self._graph.replay()
+                with self._on(stream):  # replay and finish on the caller's stream
+                    self._graph.replay()
                 self._finish(keys, stream)
                 return self.keys_out, self.vals_out
             if self._graph_key != key:  # first call with this input: eager (one-time library setup)
@@ -117,10 +118,17 @@ class Sorter:
             self._graph = g
             if self._status is not None:
                 self._status.zero_()
-            g.replay()
+            with self._on(stream):
+                g.replay()
             self._finish(keys, stream)
             return self.keys_out, self.vals_out
         return self._run(keys, vin, stream)
+
+    @staticmethod
+    def _on(stream):
+        import contextlib
+
+        return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
     def _run_async(self, keys, vin):
         lib = _lib.load()

@@ -707,3 +707,25 @@ def test_counting_pass_graph_replay_and_reuse(cuda, oracle):
             got, _ = s(t)
             torch.cuda.synchronize()
             assert np.array_equal(got.cpu().numpy().view(np.uint32), np.sort(k))
+
+
+@pytest.mark.parametrize("algorithm", ["radix", "bucket"])
+def test_graph_replay_on_caller_stream(cuda, oracle, algorithm):
+    """Sorter(graph=True) called with an explicit stream: the replay, the bucket
+    status read and its finish all run on that stream."""
+    import torch
+
+    from paper_1206_3511_b200 import device
+
+    n = 300_007
+    k = oracle.uniform_u32(n, 11)
+    t = torch.from_numpy(k.view(np.int32)).cuda()
+    s = device.Sorter(n, 4, algorithm, "iota", graph=True)
+    want_k, want_i = oracle.sort_u32(k, with_index=True)
+    st = torch.cuda.Stream()
+    for _ in range(4):
+        st.wait_stream(torch.cuda.current_stream())
+        ko, vo = s(t, stream=st)
+        st.synchronize()
+        assert np.array_equal(ko.cpu().numpy().view(np.uint32), want_k)
+        assert np.array_equal(vo.cpu().numpy().view(np.uint32), want_i)
