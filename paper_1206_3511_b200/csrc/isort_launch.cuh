@@ -213,36 +213,30 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
         launch_passes<K, VALS, Dz, PassCfg<K, VALS, ISORT_PASS_CHUNKS>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
                                                         dz, s);
     launched(D);
+    // the plan's early-out shapes (radix_onesweep.cuh, k_finish_a / k_finish_b): sorted
+    // copy, run-wise reversal, counting pass -- each kernel returns at once unless chosen
     const uint64_t cblocks = (n + 4095) / 4096;
-    const unsigned cgrid = static_cast<unsigned>(cblocks < 4ull * sm_count() ? (cblocks ? cblocks : 1) : 4ull * sm_count());
-    k_copy_if_unsorted_skip<K><<<cgrid, 512, 0, s>>>(kin, kout, vin, VALS ? vout : nullptr, iota ? 1 : 0, n, st);
-    prof_mark(s, "copy");
-    // non-increasing input (the plan's reverse early-out): the run-wise reversal
-    if (!VALS) {
-        k_reverse_keys<K><<<cgrid, 512, 0, s>>>(kin, kout, n, st);
-        launched(2);
-    } else {
-        // the look-back rows are unused on this path: they hold the long-run list
-        // (at most n / (kRevShortRun + 1) runs of 16 bytes, well inside the rows)
-        auto* long_runs = static_cast<unsigned long long*>(lookback);
-        const unsigned rgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
-        k_reverse_pairs<K><<<cgrid, 512, 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st);
-        k_rev_fix_runs<K><<<cgrid, 512, 0, s>>>(kout, vout, n, st, long_runs);
-        k_rev_long_runs<<<rgrid, 512, 0, s>>>(vout, st, long_runs);
-        launched(3);
+    const unsigned fgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
+    CountState* cs = count_state(st);
+    // the look-back rows are unused on the early-out paths: they hold the reversal's
+    // long-run list (at most n / (kRevShortRun + 1) runs of 16 bytes, inside the rows)
+    auto* long_runs = static_cast<unsigned long long*>(lookback);
+    const bool counting = !VALS && (plan_flags & kPlanCounting);
+    constexpr size_t kHistSmem = static_cast<size_t>(kCountBins) * kCountRep * sizeof(uint32_t);
+    auto* fa = k_finish_a<K, VALS>;
+    if (counting) set_max_smem_once(fa, kHistSmem);
+    fa<<<fgrid, kCountBlock, counting ? kHistSmem : 0, s>>>(kin, kout, vin, vout, iota ? 1 : 0, n, st, cs);
+    prof_mark(s, "finish_a");
+    launched(1);
+    if (counting || VALS) {
+        k_finish_b<K, VALS><<<fgrid, kCountBlock, 0, s>>>(kout, vout, n, st, cs, long_runs);
+        prof_mark(s, "finish_b");
+        launched(1);
     }
-    prof_mark(s, "reverse");
-    if (plan_flags & kPlanCounting) {  // small key range (K6): counts + fill, if the plan chose it
-        CountState* cs = count_state(st);
-        constexpr size_t kHistSmem = static_cast<size_t>(kCountBins) * kCountRep * sizeof(uint32_t);
-        auto* kh = k_count_hist<K>;
-        set_max_smem_once(kh, kHistSmem);
-        const unsigned hgrid = static_cast<unsigned>(cblocks < 2ull * sm_count() ? (cblocks ? cblocks : 1) : 2ull * sm_count());
-        kh<<<hgrid, kCountBlock, kHistSmem, s>>>(kin, n, st, cs);
-        prof_mark(s, "count_hist");
-        k_count_fill<K><<<hgrid, kCountBlock, 0, s>>>(kout, n, st, cs);
-        prof_mark(s, "count_fill");
-        launched(2);
+    if (VALS) {
+        k_rev_long_runs<<<fgrid, 512, 0, s>>>(vout, st, long_runs);
+        prof_mark(s, "rev_long");
+        launched(1);
     }
     ISORT_CUDA_TRY(cudaGetLastError());
     return ISORT_OK;

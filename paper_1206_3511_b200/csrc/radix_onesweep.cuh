@@ -892,10 +892,9 @@ static __global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations
 
 // ------------------------------------------------------------------- K4
 template <typename K>
-__global__ void k_copy_if_unsorted_skip(const K* __restrict__ in, K* __restrict__ out,
+__device__ __forceinline__ void d_copy_in_to_out(const K* __restrict__ in, K* __restrict__ out,
                                         const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
                                         int iota_vals, uint64_t n, const RadixState* __restrict__ st) {
-    if (!st->copy_in_to_out) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     // 16-byte vectors when both pointers are aligned (the common case), scalar tail
@@ -927,10 +926,9 @@ constexpr int kCountBlock = 1024;
 constexpr int kCountRep = 4;  // counter copies per bin (lane % kCountRep): fewer same-address lanes
 
 template <typename K>
-__global__ void __launch_bounds__(kCountBlock) k_count_hist(const K* __restrict__ keys, uint64_t n,
+__device__ __forceinline__ void d_count_hist(const K* __restrict__ keys, uint64_t n,
                                                             const RadixState* __restrict__ st,
                                                             CountState* __restrict__ cs) {
-    if (!st->counting) return;
     extern __shared__ __align__(16) uint32_t ch[];  // kCountBins * kCountRep
     for (int i = threadIdx.x; i < kCountBins * kCountRep; i += kCountBlock) ch[i] = 0;
     __syncthreads();
@@ -964,10 +962,9 @@ __global__ void __launch_bounds__(kCountBlock) k_count_hist(const K* __restrict_
 // writes its share of the output in 16-byte vectors: position p holds the v with
 // offs[v] <= p < offs[v + 1] (a binary search per vector, then a walk).
 template <typename K>
-__global__ void __launch_bounds__(kCountBlock, 2) k_count_fill(K* __restrict__ out, uint64_t n,
+__device__ __forceinline__ void d_count_fill(K* __restrict__ out, uint64_t n,
                                                             const RadixState* __restrict__ st,
                                                             const CountState* __restrict__ cs) {
-    if (!st->counting) return;
     __shared__ uint32_t ends[kCountBins];  // inclusive prefix: ends[v] = offs[v] + cnt[v]
     __shared__ uint32_t wtot[kCountBlock / 32];
     constexpr int kPer = kCountBins / kCountBlock;
@@ -1051,9 +1048,8 @@ __device__ __forceinline__ uint4 reverse_vec(uint4 q) {
 }
 
 template <typename K>
-__global__ void k_reverse_keys(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+__device__ __forceinline__ void d_reverse_keys(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
                                const RadixState* __restrict__ st) {
-    if (!st->reversed) return;
     constexpr uint64_t E = 16 / sizeof(K);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1067,10 +1063,9 @@ __global__ void k_reverse_keys(const K* __restrict__ in, K* __restrict__ out, ui
 }
 
 template <typename K>
-__global__ void k_reverse_pairs(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
+__device__ __forceinline__ void d_reverse_pairs(const K* __restrict__ kin, K* __restrict__ kout, const uint32_t* __restrict__ vin,
                                 uint32_t* __restrict__ vout, int iota_vals, uint64_t n,
                                 const RadixState* __restrict__ st) {
-    if (!st->reversed) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool aligned = ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(kout) |
@@ -1109,9 +1104,8 @@ __device__ __forceinline__ uint64_t run_end(const K* __restrict__ keys, uint64_t
 }
 
 template <typename K>
-__global__ void k_rev_fix_runs(const K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
+__device__ __forceinline__ void d_rev_fix_runs(const K* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t n,
                                RadixState* __restrict__ st, unsigned long long* __restrict__ long_runs) {
-    if (!st->reversed) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const bool vec = sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(keys) & 15u) == 0;
     // a thread checks positions [4g, 4g + 4) per step: one 16-byte load of them plus
@@ -1167,6 +1161,40 @@ static __global__ void k_rev_long_runs(uint32_t* __restrict__ vals, const RadixS
             vals[e - 1 - j] = t;
         }
     }
+}
+
+// The plan's early-out shapes as two launches (every one returns at once unless
+// the plan chose its shape; small sorts replay fewer graph nodes):
+//   k_finish_a  sorted: copy | non-increasing: reversal (keys, or keys + payload) |
+//               small key range (keys only): value histogram
+//   k_finish_b  small key range: fill | non-increasing with payload: run fix-up
+// (k_rev_long_runs follows for payloads: runs longer than kRevShortRun.)
+template <typename K, bool VALS>
+__global__ void __launch_bounds__(kCountBlock) k_finish_a(const K* __restrict__ kin, K* __restrict__ kout,
+                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ vout,
+                                                          int iota_vals, uint64_t n, const RadixState* __restrict__ st,
+                                                          CountState* __restrict__ cs) {
+    if (st->copy_in_to_out) {
+        d_copy_in_to_out<K>(kin, kout, vin, VALS ? vout : nullptr, iota_vals, n, st);
+    } else if (st->reversed) {
+        if (VALS)
+            d_reverse_pairs<K>(kin, kout, vin, vout, iota_vals, n, st);
+        else
+            d_reverse_keys<K>(kin, kout, n, st);
+    } else if (!VALS && st->counting) {
+        d_count_hist<K>(kin, n, st, cs);
+    }
+}
+
+template <typename K, bool VALS>
+__global__ void __launch_bounds__(kCountBlock, 2) k_finish_b(K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                             uint64_t n, RadixState* __restrict__ st,
+                                                             const CountState* __restrict__ cs,
+                                                             unsigned long long* __restrict__ long_runs) {
+    if (!VALS && st->counting)
+        d_count_fill<K>(kout, n, st, cs);
+    else if (VALS && st->reversed)
+        d_rev_fix_runs<K>(kout, vout, n, st, long_runs);
 }
 
 }  // namespace isort

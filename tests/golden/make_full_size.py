@@ -3,7 +3,7 @@ its stated size (test infrastructure; run where /root/reference was compiled):
 
     python tests/golden/make_full_size.py            # writes full_size_checksums.json
 
-C2, C3, C4a (10^8 keys) and C4b (C4a reversed, tags = positions) are sorted by the
+C1 (10^6 keys), C2, C3, C4a (10^8 keys) and C4b (C4a reversed, tags = positions) are sorted by the
 UNMODIFIED reference (oracle/_ref/libintsort_ref.so): radix_sort_lsd at base 256
 (proj/core/src/sort.cpp:112-119) and, as a cross-check, bucket_sort with the
 config's range bound (sort.cpp:136-152); the two agree by construction (both are
@@ -48,8 +48,9 @@ def entry(keys_in, keys_out, pos_out, source, **extra):
 def main(which=None) -> None:
     ref, orc = Reference(), Oracle()
     res = json.load(open(OUT)) if os.path.exists(OUT) else {}
-    n = 100_000_000
+    sizes = {"c1": 1_000_000}  # the CPU-runnable config; the others are 10^8
     specs = {
+        "c1": (1, U32_MAX),
         "c2": (1, U32_MAX),
         "c3": (1, 1023),
         "c4a": (2, U32_MAX),
@@ -59,6 +60,7 @@ def main(which=None) -> None:
         if which and name not in which:
             continue
         t0 = time.time()
+        n = sizes.get(name, 100_000_000)
         seq = ref.generate(case_id, n, bound, 42)
         if name == "c4b":
             seq = seq[::-1].copy()

@@ -20,8 +20,8 @@ def sha(a):
 def test_every_config_has_a_reference_checksum():
     with open(os.path.join(GOLDEN, "full_size_checksums.json")) as f:
         c = json.load(f)
-    assert set(c) == {"c2", "c3", "c4a", "c4b", "c5"}
-    assert c["c5"]["n"] == 10**9 and all(c[k]["n"] == 10**8 for k in ("c2", "c3", "c4a", "c4b"))
+    assert set(c) == {"c1", "c2", "c3", "c4a", "c4b", "c5"}
+    assert c["c5"]["n"] == 10**9 and c["c1"]["n"] == 10**6 and all(c[k]["n"] == 10**8 for k in ("c2", "c3", "c4a", "c4b"))
     assert "reference radix_sort_lsd" in c["c2"]["source"]
 
 

@@ -60,7 +60,7 @@ def sort_on_device(keys: np.ndarray, algorithm: str, payload, bound: int):
     return ko, vo
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4a", "c4b", "c5"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4a", "c4b", "c5"])
 def test_full_size_bit_exact(cuda, oracle, checks, cfg):
     c = checks[cfg]
     keys = config_input(cfg, oracle)

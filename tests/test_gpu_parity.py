@@ -668,11 +668,12 @@ def test_is_sorted_u32(cuda, n):
 
 
 # ------------------------------------------------------- small key range: the counting pass (K6)
-@pytest.mark.parametrize("n", [1, 2, 5, 4097, 100_003, 3_000_001])
+@pytest.mark.parametrize("n", [1, 2, 5, 4097, 100_003, 4_194_304, 5_000_011])
 @pytest.mark.parametrize("top", [2, 1023, 4095, 4096])
 def test_counting_pass_small_range(cuda, oracle, n, top):
-    """Keys-only sorts with every key < 2^12 take one counting pass (histogram +
-    fill) -- radix always, bucket when M < 2^12 <= n (one value per bucket).
+    """Keys-only sorts of at least 2^22 keys with every key < 2^12 take one
+    counting pass (histogram + fill) -- radix always, bucket when M < 2^12 <= n
+    (one value per bucket); smaller ones the digit passes.
     max = 4096 must take the digit passes.  Bit-exact against the oracle; with a
     payload the same inputs take the stable scatter."""
     rng = np.random.default_rng(n * 7 + top)
@@ -696,7 +697,7 @@ def test_counting_pass_graph_replay_and_reuse(cuda, oracle):
 
     from paper_1206_3511_b200 import device
 
-    n = 1_000_003
+    n = 4_200_001
     small = oracle.uniform_u32(n, 3) & np.uint32(1023)
     wide = oracle.uniform_u32(n, 4)
     s = device.Sorter(n, 4, "radix", None, graph=True)
