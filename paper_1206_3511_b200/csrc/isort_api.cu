@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -23,6 +24,9 @@
 #include <vector>
 
 #include <unistd.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "../../include/isort.h"
 #include "bucket_sort.cuh"
@@ -360,6 +364,39 @@ __global__ void k_gather_records(const isort_record* __restrict__ in, const uint
 // across calls) and issue its DMA on their own stream, so host copies, PCIe
 // transfers in both directions and per-chunk device work (the key pack) overlap.
 constexpr size_t kStageChunk = 16u << 20;  // bytes per chunk (a multiple of 16 B records)
+
+// Host copy for the staging path with non-temporal (streaming) stores: the
+// destination lines are not read first (no read-for-ownership) and do not
+// displace the cache, which matters when every core copies at once and the
+// host's memory bandwidth is the limit (the DMA uses it too).
+inline void stream_copy(void* dst, const void* src, size_t bytes) {
+#if defined(__SSE2__)
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15u)) & 15u;
+    if (bytes < head + 64) {
+        std::memcpy(d, s, bytes);
+        return;
+    }
+    std::memcpy(d, s, head);
+    d += head, s += head, bytes -= head;
+    const size_t body = bytes & ~static_cast<size_t>(63);
+    for (size_t i = 0; i < body; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+        const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+    }
+    _mm_sfence();
+    std::memcpy(d + body, s + body, bytes - body);
+#else
+    std::memcpy(dst, src, bytes);
+#endif
+}
 constexpr int kStageSlots = 2;             // per worker
 
 struct Staging {
@@ -432,7 +469,7 @@ int upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s, Stag
             const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
             const int slot = w * kStageSlots + k;
             ISORT_CUDA_TRY(cudaEventSynchronize(st.slot_done[slot]));  // its previous DMA has read it
-            std::memcpy(st.slots[slot], static_cast<const char*>(src) + off, len);
+            stream_copy(st.slots[slot], static_cast<const char*>(src) + off, len);
             ISORT_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.slots[slot], len,
                                            cudaMemcpyHostToDevice, ws));
             ISORT_CUDA_TRY(cudaEventRecord(st.slot_done[slot], ws));
@@ -475,7 +512,7 @@ int download_staged(void* dst, const void* src, size_t bytes, cudaStream_t s, St
             }
             if (prev_slot >= 0) {
                 ISORT_CUDA_TRY(cudaEventSynchronize(st.slot_done[prev_slot]));
-                std::memcpy(static_cast<char*>(dst) + prev_off, st.slots[prev_slot], prev_len);
+                stream_copy(static_cast<char*>(dst) + prev_off, st.slots[prev_slot], prev_len);
             }
             if (!more) break;
             prev_slot = slot;
@@ -493,9 +530,9 @@ int download_staged(void* dst, const void* src, size_t bytes, cudaStream_t s, St
 // keys_out, idx_out, n, s)` run the u32 / u64 pipelines.  One host read per call:
 // the max key after the upload decides u32 or u64 keys (the sort cannot start
 // before the last chunk has arrived anyway).
-template <typename Sort32, typename Sort64>
+template <typename Sort32, typename Sort64, typename Temp32, typename Temp64>
 int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t n, int device, Sort32&& sort32,
-                            Sort64&& sort64) {
+                            Sort64&& sort64, Temp32&& temp32, Temp64&& temp64) {
     cudaStream_t s;
     int rc = use_device(device, &s);
     if (rc) return rc;
@@ -508,15 +545,26 @@ int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t 
         if ((rc = staging_for(device, &stg))) return rc;
     }
     std::lock_guard<std::mutex> g(stg->mu);
-    DevBuf rec_in, rec_out, keys, keys_out, idx, maxw;
-    if ((rc = rec_in.alloc(n * sizeof(isort_record), s)) || (rc = rec_out.alloc(n * sizeof(isort_record), s)) ||
-        (rc = keys.alloc(n * sizeof(uint64_t), s)) || (rc = keys_out.alloc(n * sizeof(uint64_t), s)) ||
+    // Device memory: the records (16n), the positions (4n) and one scratch region that
+    // holds keys, sorted keys and the sort's temp, and then -- once only the positions
+    // are needed -- the gathered output records (16n).  Peak ~36n bytes for u32 keys
+    // (3.6 GB at 10^8), inside the pool's kept memory, so repeated calls map nothing.
+    const size_t rec_bytes = n * sizeof(isort_record);
+    const size_t k32_bytes = align_up(n * sizeof(uint32_t));
+    const size_t scratch32 = std::max(rec_bytes, 2 * k32_bytes + temp32(n));
+    DevBuf rec_in, scratch, idx, maxw;
+    if ((rc = rec_in.alloc(rec_bytes, s)) || (rc = scratch.alloc(scratch32, s)) ||
         (rc = idx.alloc(n * sizeof(uint32_t), s)) || (rc = maxw.alloc(sizeof(unsigned long long), s)))
         return rc;
     ISORT_CUDA_TRY(cudaMemsetAsync(maxw.p, 0, sizeof(unsigned long long), s));
     auto* rin = rec_in.as<isort_record>();
-    auto* k32 = keys.as<uint32_t>();
+    auto* k32 = scratch.as<uint32_t>();
     auto* mxp = maxw.as<unsigned long long>();
+    // ISORT_HOST_TRACE=1: wall-clock split of the call on stderr (upload, sort, download)
+    static const bool trace = [] { const char* e = std::getenv("ISORT_HOST_TRACE"); return e && e[0] == '1'; }();
+    const auto now = [] { return std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = trace ? now() : 0.0;
     rc = upload_staged(rin, in, n * sizeof(isort_record), s, *stg, [&](cudaStream_t ws, size_t off, size_t len) {
         const uint64_t lo = off / sizeof(isort_record), m = len / sizeof(isort_record);
         k_pack_records_u32<<<grid_for(m), 256, 0, ws>>>(rin + lo, k32 + lo, m, mxp);
@@ -527,30 +575,47 @@ int sort_records_via_device(const isort_record* in, isort_record* out, uint64_t 
     unsigned long long mx = 0;
     ISORT_CUDA_TRY(cudaMemcpyAsync(&mx, maxw.p, sizeof mx, cudaMemcpyDeviceToHost, s));
     ISORT_CUDA_TRY(cudaStreamSynchronize(s));
+    const double t1 = trace ? now() : 0.0;
+    char* sc = scratch.as<char>();
+    DevBuf scratch64;  // 40-bit keys (the generator's 2^40 bound): a larger scratch
     if (mx <= 0xffffffffull) {
-        rc = sort32(k32, keys_out.as<uint32_t>(), idx.as<uint32_t>(), n, s);
+        rc = sort32(k32, reinterpret_cast<uint32_t*>(sc + k32_bytes), idx.as<uint32_t>(), n, sc + 2 * k32_bytes, s);
     } else {
-        k_pack_records_u64<<<grid_for(n), 256, 0, s>>>(rin, keys.as<uint64_t>(), n);
+        const size_t k64_bytes = align_up(n * sizeof(uint64_t));
+        if ((rc = scratch64.alloc(std::max(rec_bytes, 2 * k64_bytes + temp64(n)), s))) return rc;
+        sc = scratch64.as<char>();
+        auto* k64 = reinterpret_cast<uint64_t*>(sc);
+        k_pack_records_u64<<<grid_for(n), 256, 0, s>>>(rin, k64, n);
         launched();
-        rc = sort64(keys.as<uint64_t>(), keys_out.as<uint64_t>(), idx.as<uint32_t>(), n, s);
+        rc = sort64(k64, reinterpret_cast<uint64_t*>(sc + k64_bytes), idx.as<uint32_t>(), n, sc + 2 * k64_bytes, s);
     }
     if (rc) {
         cudaStreamSynchronize(s);
         return rc;
     }
-    k_gather_records<<<grid_for(n), 256, 0, s>>>(rin, idx.as<uint32_t>(), rec_out.as<isort_record>(), n);
+    auto* rec_out = reinterpret_cast<isort_record*>(sc);  // the keys and temp are dead now
+    k_gather_records<<<grid_for(n), 256, 0, s>>>(rin, idx.as<uint32_t>(), rec_out, n);
     launched();
     ISORT_CUDA_TRY(cudaGetLastError());
-    return download_staged(out, rec_out.p, n * sizeof(isort_record), s, *stg);
+    double t2 = 0.0;
+    if (trace) {
+        cudaStreamSynchronize(s);
+        t2 = now();
+    }
+    rc = download_staged(out, rec_out, rec_bytes, s, *stg);
+    if (trace)
+        std::fprintf(stderr, "isort records n=%llu workers=%d: upload+pack %.1f ms, sort+gather %.1f ms, download %.1f ms\n",
+                     (unsigned long long)n, stg->workers, t1 - t0, t2 - t1, now() - t2);
+    return rc;
 }
 
+// (key, position) sort for the records path; `temp` (pairs_temp_bytes) comes from the caller.
 template <typename K>
-int radix_pairs_owned(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, cudaStream_t s) {
-    const size_t tb = radix_layout<K>(n, true).total;
-    DevBuf temp;
-    int rc = temp.alloc(tb, s);
-    if (rc) return rc;
-    return radix_sort_device<K>(keys, keys_out, nullptr, idx, n, ISORT_VALS_IOTA, temp.p, tb, s);
+size_t radix_pairs_temp_bytes(uint64_t n) { return radix_layout<K>(n, true).total; }
+template <typename K>
+int radix_pairs(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, void* temp, cudaStream_t s) {
+    return radix_sort_device<K>(keys, keys_out, nullptr, idx, n, ISORT_VALS_IOTA, temp, radix_pairs_temp_bytes<K>(n),
+                                s);
 }
 
 __global__ void k_max_records(const isort_record* __restrict__ rec, uint64_t n, unsigned long long* __restrict__ out) {
@@ -821,12 +886,11 @@ int bucket_sort_impl(const K* kin, K* kout, const uint32_t* vin, uint32_t* vout,
 }
 
 template <typename K>
-int bucket_pairs_owned(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, uint64_t bound, cudaStream_t s) {
-    const size_t tb = bucket_layout<K>(n, true).total;
-    DevBuf temp;
-    int rc = temp.alloc(tb, s);
-    if (rc) return rc;
-    return bucket_sort_device<K>(keys, keys_out, nullptr, idx, n, bound, ISORT_VALS_IOTA, temp.p, tb, s);
+size_t bucket_pairs_temp_bytes(uint64_t n) { return bucket_layout<K>(n, true).total; }
+template <typename K>
+int bucket_pairs(const K* keys, K* keys_out, uint32_t* idx, uint64_t n, uint64_t bound, void* temp, cudaStream_t s) {
+    return bucket_sort_device<K>(keys, keys_out, nullptr, idx, n, bound, ISORT_VALS_IOTA, temp,
+                                 bucket_pairs_temp_bytes<K>(n), s);
 }
 
 template <typename K>
@@ -1125,12 +1189,13 @@ int isort_radix_sort_records(const isort_record* in, isort_record* out, uint64_t
     if (!in || !out) return set_error(ISORT_EINVAL, "isort_radix_sort_records: null buffer");
     return sort_records_via_device(
         in, out, n, device,
-        [](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
-            return radix_pairs_owned<uint32_t>(k, ko, idx, m, s);
+        [](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, void* t, cudaStream_t s) {
+            return radix_pairs<uint32_t>(k, ko, idx, m, t, s);
         },
-        [](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
-            return radix_pairs_owned<uint64_t>(k, ko, idx, m, s);
-        });
+        [](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, void* t, cudaStream_t s) {
+            return radix_pairs<uint64_t>(k, ko, idx, m, t, s);
+        },
+        radix_pairs_temp_bytes<uint32_t>, radix_pairs_temp_bytes<uint64_t>);
 }
 
 int isort_bucket_sort_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t range_bound,
@@ -1140,12 +1205,13 @@ int isort_bucket_sort_records(const isort_record* in, isort_record* out, uint64_
     if (!in || !out) return set_error(ISORT_EINVAL, "isort_bucket_sort_records: null buffer");
     return sort_records_via_device(
         in, out, n, device,
-        [range_bound](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
-            return bucket_pairs_owned<uint32_t>(k, ko, idx, m, range_bound, s);
+        [range_bound](const uint32_t* k, uint32_t* ko, uint32_t* idx, uint64_t m, void* t, cudaStream_t s) {
+            return bucket_pairs<uint32_t>(k, ko, idx, m, range_bound, t, s);
         },
-        [range_bound](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, cudaStream_t s) {
-            return bucket_pairs_owned<uint64_t>(k, ko, idx, m, range_bound, s);
-        });
+        [range_bound](const uint64_t* k, uint64_t* ko, uint32_t* idx, uint64_t m, void* t, cudaStream_t s) {
+            return bucket_pairs<uint64_t>(k, ko, idx, m, range_bound, t, s);
+        },
+        bucket_pairs_temp_bytes<uint32_t>, bucket_pairs_temp_bytes<uint64_t>);
 }
 
 int isort_counting_sort_by_digit_records(const isort_record* in, isort_record* out, uint64_t n, uint64_t base,
