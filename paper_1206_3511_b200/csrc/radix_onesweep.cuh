@@ -882,9 +882,20 @@ static __global__ void k_selftest_atomic_order(uint32_t* __restrict__ violations
         v = v * 1664525u + 1013904223u;
         const uint32_t mod = 1u + ((v >> 8) & 31u);
         const uint32_t d = (lane * 2654435761u + v) % mod * 7u % 256u;
+        // (1) the one-sweep rank: atomicAdd(p, 1) with the old value (ATOMS.POPC.INC)
         const uint32_t old = atomicAdd(&wh[d], 1u);
         const uint32_t peers = __match_any_sync(ISORT_FULL_MASK, d);
-        bad += (old != static_cast<uint32_t>(__popc(peers & lanemask_lt())));
+        const uint32_t want = static_cast<uint32_t>(__popc(peers & lanemask_lt()));
+        bad += (old != want);
+        __syncwarp();
+        for (int i = lane; i < 257; i += 32) wh[i] = 0;
+        __syncwarp();
+        // (2) the segment sort's rank: two 16-bit counters per word, increment
+        // 1 << 16 for odd digits (a plain ATOMS.ADD); lanes whose digits share a
+        // word contend, and the lanes of one digit must still be served in order
+        const uint32_t hsh = (d & 1u) << 4;
+        const uint32_t old2 = (atomicAdd(&wh[d >> 1], 1u << hsh) >> hsh) & 0xFFFFu;
+        bad += (old2 != want);
         __syncwarp();
     }
     if (bad) atomicAdd(violations, bad);

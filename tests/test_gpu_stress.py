@@ -2,7 +2,8 @@
 payload, algorithm, graph) combinations against numpy's stable argsort.  Sizes
 straddle every tile shape (small-n 1-chunk tiles, 2-chunk tiles, payload tiles)
 and segment-stage boundary; distributions include runs, few distinct values,
-clustered and bucket-skewed keys."""
+clustered and bucket-skewed keys, keys below 2^12 (counting pass) and
+non-increasing keys with runs (run-wise reversal)."""
 from __future__ import annotations
 
 import os
@@ -16,7 +17,7 @@ U32_MAX = (1 << 32) - 1
 
 
 def draw_keys(rng, n):
-    kind = rng.integers(0, 8)
+    kind = rng.integers(0, 10)
     if kind == 0:
         k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
     elif kind == 1:  # few distinct values
@@ -34,8 +35,12 @@ def draw_keys(rng, n):
     elif kind == 6:  # heavy duplicate + uniform
         k = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
         k[rng.random(n) < 0.4] = int(rng.integers(0, 1 << 32))
-    else:  # normal-ish
+    elif kind == 7:  # normal-ish
         k = np.clip(np.rint(2.0**31 + 2.0**24 * rng.standard_normal(n)), 0, U32_MAX).astype(np.uint64)
+    elif kind == 8:  # every key below 2^12 (the counting pass, keys only, n >= 2^22)
+        k = rng.integers(0, int(rng.integers(1, 4097)), size=n, dtype=np.uint64)
+    else:  # non-increasing with runs of equal keys (the run-wise reversal)
+        k = np.sort(rng.integers(0, max(1, n // int(rng.integers(1, 50))), size=n, dtype=np.uint64))[::-1].copy()
     return k.astype(np.uint32)
 
 

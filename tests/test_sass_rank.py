@@ -1,6 +1,7 @@
 """The one-sweep rank's stability rests on one instruction: a returning shared
-atomic add (SASS ATOMS.ADD) whose same-address lanes are granted in ascending
-lane order.  k_selftest_atomic_order re-checks that property at load time, so it
+atomic add (SASS ATOMS.ADD with a destination register; the non-returning counts
+compile to ATOMS.POPC.INC.32 RZ) whose same-address lanes are granted in
+ascending lane order.  k_selftest_atomic_order re-checks that property at load time, so it
 must exercise the SAME instruction the rank compiles to.  This CPU test
 disassembles libisort.so (cuobjdump) and pins:
   * the fast pass (SAFE = false) ranks with ATOMS.ADD and has no MATCH,
@@ -34,9 +35,12 @@ def sass_ops():
         if m:
             fn = m.group(1)
             continue
-        m = re.search(r"\b(ATOMS\.[A-Z0-9.]+|MATCH\.[A-Z]+)", line)
+        m = re.search(r"\b(ATOMS\.[A-Z0-9.]+|MATCH\.[A-Z]+)\s+(\w+)", line)
         if m and fn:
-            ops[fn][m.group(1)] += 1
+            op = m.group(1)
+            if op.startswith("ATOMS") and m.group(2) != "RZ":
+                op += ".RET"  # returns the old value: a rank, not a count
+            ops[fn][op] += 1
     return ops
 
 
@@ -47,16 +51,20 @@ def _find(ops, *parts):
 
 
 def test_fast_rank_is_returning_shared_atomic(sass_ops):
-    # k_onesweep<u32, RadixDigitizer<u32>, 512, 24, 2, VALS=0, SAFE=0, SCATTER=0, LW>
+    # k_onesweep<u32, RadixDigitizer<u32>, 512, 24, 2, VALS=0, SAFE=0, SCATTER=0, LW>: the rank is a
+    # returning ATOMS.ADD; the counts are non-returning (ATOMS.POPC.INC.32 RZ / ATOMS.ADD RZ)
     for f in _find(sass_ops, "k_onesweep", "RadixDigitizerIj", "Li512ELi24ELi2ELb0ELb0ELb0E"):
         c = sass_ops[f]
-        assert c["ATOMS.ADD"] > 0, f
+        assert c["ATOMS.ADD.RET"] > 0, (f, dict(c))
         assert not any(k.startswith("MATCH") for k in c), f
+        assert not any(k.endswith(".RET") and k != "ATOMS.ADD.RET" for k in c), (f, dict(c))
 
 
 def test_selftest_checks_the_same_instruction(sass_ops):
-    (f,) = _find(sass_ops, "k_selftest_atomic_order")
-    assert sass_ops[f]["ATOMS.ADD"] > 0 and sass_ops[f]["MATCH.ANY"] > 0
+    # both rank forms (plain +1, and the segment sort's 16-bit packed increment) as
+    # returning ATOMS.ADD, against MATCH.ANY
+    for f in _find(sass_ops, "k_selftest_atomic_order"):
+        assert sass_ops[f]["ATOMS.ADD.RET"] >= 2 and sass_ops[f]["MATCH.ANY"] > 0, (f, dict(sass_ops[f]))
 
 
 def test_safe_rank_uses_match(sass_ops):
@@ -66,4 +74,4 @@ def test_safe_rank_uses_match(sass_ops):
 
 def test_segment_sort_rank(sass_ops):
     for f in _find(sass_ops, "k_bucket_segments"):
-        assert sass_ops[f]["ATOMS.ADD"] > 0, f
+        assert sass_ops[f]["ATOMS.ADD.RET"] > 0, f
