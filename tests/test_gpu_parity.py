@@ -341,10 +341,10 @@ def test_bucket_span_errors(cuda):
 
 @pytest.mark.parametrize("n", [5000, 8191, 8192, 8193, 20_000, 100_003, 1_000_003])
 def test_bucket_segment_kernel_paths(cuda, oracle, n):
-    """The segment kernel's in-stage choices: sort by bucket + per-bucket
-    insertion (short runs, duplicates inside a bucket), the run-cap fallback to a
-    key sort (long runs of distinct keys), stages cut inside a super-bucket, and
-    tight clusters (many keys per bucket next to empty stretches)."""
+    """The segment kernel's in-stage shapes: stages of many small super-buckets
+    (narrow keys), duplicates inside a bucket (triples), stages cut inside a
+    super-bucket and tight clusters next to empty stretches (clusters: oversized
+    super-buckets, constant or re-sorted by the radix fallback)."""
     rng = np.random.default_rng(n)
     cases = {
         "narrow": rng.integers(0, 1 << 20, size=n, dtype=np.uint64).astype(np.uint32),

@@ -16,6 +16,15 @@
 
 using namespace isort;
 
+#ifndef OLD_BLOCK
+#define OLD_BLOCK 512
+#endif
+#ifndef OLD_IPT
+#define OLD_IPT 24
+#endif
+#ifndef OLD_IPTV
+#define OLD_IPTV 12
+#endif
 #ifndef EXP_BLOCK
 #define EXP_BLOCK 512
 #endif
@@ -62,6 +71,20 @@ __global__ void k_unsorted(const uint32_t* a, uint64_t n, unsigned long long* ba
     if (c) atomicAdd(bad, c);
 }
 
+// keys sorted; with positions: kin[pos[i]] == kout[i] and positions ascending inside runs
+__global__ void k_check(const uint32_t* kin, const uint32_t* kout, const uint32_t* pos, uint64_t n,
+                        unsigned long long* bad) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i + 1 < n && kout[i] > kout[i + 1]) ++c;
+        if (pos) {
+            if (kin[pos[i]] != kout[i]) ++c;
+            if (i + 1 < n && kout[i] == kout[i + 1] && pos[i] >= pos[i + 1]) ++c;
+        }
+    }
+    if (c) atomicAdd(bad, c);
+}
+
 int main(int argc, char** argv) {
     const uint64_t n = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 100000000ull;
     const int vmode = argc > 2 ? std::atoi(argv[2]) : 0;
@@ -95,11 +118,11 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)uf_smem));
 
     // v10 pass
-    constexpr int kOldIpt = 24, kOldIptV = 12;
-    using OldSm = OnesweepSmem<uint32_t, 512, kOldIpt, 2, false, false>;
-    using OldSmV = OnesweepSmem<uint32_t, 512, kOldIptV, 2, true, false>;
-    auto* kold = k_onesweep<uint32_t, RadixDigitizer<uint32_t>, 512, kOldIpt, 2, false, false, false>;
-    auto* koldv = k_onesweep<uint32_t, RadixDigitizer<uint32_t>, 512, kOldIptV, 2, true, false, false>;
+    constexpr int kOldIpt = OLD_IPT, kOldIptV = OLD_IPTV;
+    using OldSm = OnesweepSmem<uint32_t, OLD_BLOCK, kOldIpt, 2, false, false>;
+    using OldSmV = OnesweepSmem<uint32_t, OLD_BLOCK, kOldIptV, 2, true, false>;
+    auto* kold = k_onesweep<uint32_t, RadixDigitizer<uint32_t>, OLD_BLOCK, kOldIpt, 2, false, false, false>;
+    auto* koldv = k_onesweep<uint32_t, RadixDigitizer<uint32_t>, OLD_BLOCK, kOldIptV, 2, true, false, false>;
     CK(cudaFuncSetAttribute(kold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OldSm)));
     CK(cudaFuncSetAttribute(koldv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OldSmV)));
     // v2 pass
@@ -120,7 +143,7 @@ int main(int argc, char** argv) {
                                                      vals ? sizeof(P2SmV) : sizeof(P2Sm)));
     std::printf("v2b: ipt %d smem %zu occ %d\n", vals ? EXP_IPT2V : EXP_IPT2, vals ? sizeof(P2SmV) : sizeof(P2Sm), occ_p2);
     int occ_old = 0, occ_new = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_old, vals ? koldv : kold, 512,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_old, vals ? koldv : kold, OLD_BLOCK,
                                                      vals ? sizeof(OldSmV) : sizeof(OldSm)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_new, vals ? knewv : knew, EXP_BLOCK,
                                                      vals ? sizeof(NewSmV) : sizeof(NewSm)));
@@ -134,7 +157,7 @@ int main(int argc, char** argv) {
         const bool use_new = variant != 0;
         const int tile = variant == 2 ? EXP_BLOCK * (vals ? EXP_IPT2V : EXP_IPT2)
                          : use_new    ? EXP_BLOCK * (vals ? EXP_IPTV : EXP_IPT)
-                                      : 512 * (vals ? kOldIptV : kOldIpt) * 2;
+                                      : OLD_BLOCK * (vals ? kOldIptV : kOldIpt) * 2;
         const uint32_t tiles = (uint32_t)((n + tile - 1) / tile);
         CK(cudaMemsetAsync(st, 0, sizeof(RadixState), s));
         CK(cudaMemsetAsync(lbv, 0, (size_t)4 * tiles * kRadix * (use_new ? 8 : 4), s));
@@ -162,10 +185,10 @@ int main(int argc, char** argv) {
                                                                 (unsigned long long*)lbv, tiles, p, dz, NoScatter{});
             } else {
                 if (vals)
-                    koldv<<<grid, 512, sizeof(OldSmV), s>>>(kin, kout, kalt, nullptr, vout, valt, 1, n, st,
+                    koldv<<<grid, OLD_BLOCK, sizeof(OldSmV), s>>>(kin, kout, kalt, nullptr, vout, valt, 1, n, st,
                                                             (uint32_t*)lbv, tiles, p, dz, NoScatter{});
                 else
-                    kold<<<grid, 512, sizeof(OldSm), s>>>(kin, kout, kalt, nullptr, nullptr, nullptr, 0, n, st,
+                    kold<<<grid, OLD_BLOCK, sizeof(OldSm), s>>>(kin, kout, kalt, nullptr, nullptr, nullptr, 0, n, st,
                                                           (uint32_t*)lbv, tiles, p, dz, NoScatter{});
             }
             CK(cudaEventRecord(ev[p + 1], s));
@@ -181,7 +204,12 @@ int main(int argc, char** argv) {
     uint32_t *kout_c, *vout_c;
     CK(cudaMalloc(&kout_c, n * 4));
     CK(cudaMalloc(&vout_c, n * 4));
-    for (int which = 0; which < 3; ++which) {
+#ifdef EXP_ONLY_OLD
+    constexpr int kVariants = 1;
+#else
+    constexpr int kVariants = 3;
+#endif
+    for (int which = 0; which < kVariants; ++which) {
         const bool use_new = which != 0;
         uint32_t* ko = which == 0 ? kout_a : (which == 1 ? kout_b : kout_c);
         uint32_t* vo = which == 0 ? vout_a : (which == 1 ? vout_b : vout_c);
@@ -206,6 +234,11 @@ int main(int argc, char** argv) {
                     8.0 * n / ((pm[1] + pm[2] + pm[3]) / 3 / reps * 1e-3) / 1e9 / 6453.7);
     }
     unsigned long long bad = 0;
+    CK(cudaMemset(dbad, 0, 8));
+    k_check<<<1024, 256>>>(kin, kout_a, vals ? vout_a : nullptr, n, dbad);
+    CK(cudaMemcpy(&bad, dbad, 8, cudaMemcpyDeviceToHost));
+    std::printf("v10 check (sorted, stable positions) violations: %llu\n", bad);
+    if (kVariants == 1) return 0;
     CK(cudaMemset(dbad, 0, 8));
     k_diff<<<1024, 256>>>(kout_a, kout_b, n, dbad);
     CK(cudaMemcpy(&bad, dbad, 8, cudaMemcpyDeviceToHost));
