@@ -191,7 +191,9 @@ struct BucketDigitizer {
     static constexpr bool kCheapDigit = MODE == kPow2Narrow;
     BucketIndexer bi;
     uint32_t shift[kBucketMaxDigits];  // digit p = (b >> shift[p]) & 255; unused: 63 (=> 0)
-    uint32_t s_lo;                     // super-bucket = b >> s_lo
+    uint32_t s_lo;                     // fine plan: super-bucket = b >> s_lo
+    uint32_t s_lo_coarse;              // coarse plan (lowest digit pass skipped)
+    uint32_t adaptive;                 // the lowest digit pass is optional (skew decides)
     uint32_t used;                     // number of digit passes that can be non-trivial
 
     uint32_t tsh[kBucketMaxDigits];    // kPow2Narrow: log2(M + 1) + shift[p], capped at 64 (=> 0)
@@ -223,8 +225,16 @@ struct BucketDigitizer {
         const uint32_t L = n > 1 ? 64 - __builtin_clzll(n - 1) : 0;  // bits of the largest bucket index
         uint32_t db = L > kSuperBucketBits ? (L - kSuperBucketBits + 7) / 8 : 0;
         if (db > kBucketMaxDigits) db = kBucketMaxDigits;
+        // Skewed keys: one more, finer digit pass when a slot is free.  K1 counts the
+        // fine digits; the coarse plan is the fine one without its lowest digit, so
+        // K2 decides on the device (k_plan, kPlanAdaptiveLow) and tells the segment
+        // kernel the super-bucket shift (RadixState::sb_shift).
+        const uint32_t fine = db >= 1 && db < kBucketMaxDigits ? db + 1 : db;
+        d.adaptive = fine > db ? 1u : 0u;
+        db = fine;
         d.used = db;
         d.s_lo = L > 8 * db ? L - 8 * db : 0;
+        d.s_lo_coarse = d.adaptive ? d.s_lo + 8 : d.s_lo;
         for (uint32_t p = 0; p < kBucketMaxDigits; ++p) {
             d.shift[p] = p < db ? d.s_lo + 8 * p : 63;
             const uint32_t t = (d.bi.pow2_shift < 64 ? d.bi.pow2_shift : 64) + d.shift[p];
@@ -286,8 +296,19 @@ struct BucketDigitizer {
     }
     __device__ __forceinline__ bool needs_range_check() const { return check_range != 0; }
     __device__ __forceinline__ uint64_t bucket(K key) const { return bidx(key); }
-    __device__ __forceinline__ uint64_t super_bucket(K key) const {
-        return bidx(key) >> s_lo;
+    // K2's arguments: the optional fine pass and the two super-bucket shifts
+    void plan_args(int* flags, int* top, uint32_t* top_bins, uint32_t* sb_fine, uint32_t* sb_coarse) const {
+        if (adaptive) *flags |= kPlanAdaptiveLow;
+        *top = used ? static_cast<int>(used) - 1 : 0;
+        // bins of the top digit that bucket indices < n can reach
+        const uint32_t L = bi.count > 1 ? 64 - __builtin_clzll(bi.count - 1) : 0;
+        const uint32_t hi = used ? shift[used - 1] : 0;
+        *top_bins = L > hi ? (L - hi >= 8 ? kRadix : (1u << (L - hi))) : 1u;
+        *sb_fine = s_lo;
+        *sb_coarse = s_lo_coarse;
+    }
+    __device__ __forceinline__ uint64_t super_bucket(K key, uint32_t sb_shift) const {
+        return bidx(key) >> sb_shift;
     }
 };
 
@@ -432,11 +453,12 @@ __device__ __forceinline__ uint64_t warp_first_true(uint64_t lo, uint64_t hi, Pr
 // is ordered by super-bucket after K3, so this is a lower bound: gallop from x,
 // then a 32-ary search.  Whole warp.
 template <typename K, typename Dz>
-__device__ uint64_t warp_next_start(const K* __restrict__ keys, uint64_t n, uint64_t x, const Dz& dz) {
+__device__ uint64_t warp_next_start(const K* __restrict__ keys, uint64_t n, uint64_t x, const Dz& dz,
+                                    uint32_t sbs) {
     if (x == 0) return 0;
     if (x >= n) return n;
-    const uint64_t sbp = dz.super_bucket(keys[x - 1]);
-    auto differs = [&](uint64_t i) { return dz.super_bucket(keys[i]) != sbp; };
+    const uint64_t sbp = dz.super_bucket(keys[x - 1], sbs);
+    auto differs = [&](uint64_t i) { return dz.super_bucket(keys[i], sbs) != sbp; };
     uint64_t lo = x, hi = n - x > 2048 ? x + 2048 : n;
     while (hi < n && !differs(hi - 1)) {
         lo = hi;
@@ -596,9 +618,10 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lane = lane_id();
+    const uint32_t sbs = rst->sb_shift;  // the plan's super-bucket shift (fine or coarse)
     if (warp < 2) {
         const uint64_t x = n * (blockIdx.x + static_cast<uint64_t>(warp)) / gridDim.x;
-        const uint64_t p = warp_next_start(keys, n, x, dz);
+        const uint64_t p = warp_next_start(keys, n, x, dz, sbs);
         if (lane == 0) sm.pos[warp] = p;
     }
     if (tid == 0) mbar_init(&sm.bar, 1);
@@ -641,9 +664,9 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
         if (warp == 0) {
             int l = len;
             if (!tail) {
-                const uint64_t sbl = dz.super_bucket(ka[len - 1]);
+                const uint64_t sbl = dz.super_bucket(ka[len - 1], sbs);
                 l = static_cast<int>(warp_first_true(0, static_cast<uint64_t>(len), [&](uint64_t j) {
-                    return dz.super_bucket(ka[j]) == sbl;
+                    return dz.super_bucket(ka[j], sbs) == sbl;
                 }));
             }
             if (lane == 0) sm.ls = l;
@@ -652,7 +675,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_SEG_MINB)
         int ls = sm.ls;
         if (ls == 0) {  // the whole stage is one super-bucket
             if (warp == 0) {
-                const uint64_t e = warp_next_start(keys, n, pos + len, dz);
+                const uint64_t e = warp_next_start(keys, n, pos + len, dz, sbs);
                 if (lane == 0) sm.pos[0] = e;
             }
             __syncthreads();
@@ -786,6 +809,7 @@ struct DestDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int) const { return digit_sh(key, 0u); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const { d[0] = digit_sh(key, 0u); }
     __device__ __forceinline__ bool in_range(K) const { return true; }
+    void plan_args(int*, int*, uint32_t*, uint32_t*, uint32_t*) const {}
 };
 
 static __global__ void k_copy_part_counts(const RadixState* __restrict__ st, uint64_t* __restrict__ counts, int parts) {

@@ -186,7 +186,10 @@ int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, u
     const unsigned grid1 = static_cast<unsigned>(want < cap1 ? (want ? want : 1) : cap1);
     k1<<<grid1, kUpfrontBlock, UCfg::kSmem, s>>>(kin, n, st, dz);
     prof_mark(s, "upfront");
-    k_plan<D><<<1, kRadix, 0, s>>>(st, n, plan_flags);
+    int top = 0;
+    uint32_t top_bins = kRadix, sb_fine = 0, sb_coarse = 0;
+    dz.plan_args(&plan_flags, &top, &top_bins, &sb_fine, &sb_coarse);
+    k_plan<D><<<1, kRadix, 0, s>>>(st, n, plan_flags, top, top_bins, sb_fine, sb_coarse);
     prof_mark(s, "plan");
     launched(2);
     ISORT_CUDA_TRY(cudaGetLastError());

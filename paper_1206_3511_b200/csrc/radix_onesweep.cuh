@@ -57,6 +57,7 @@ struct RadixState {
     uint32_t reversed;                  // K2: non-increasing input, out = in reversed run by run
     uint32_t counting;                  // K2: keys-only, max < kCountBins: one counting pass (K6)
     uint32_t rev_long;                  // K5: runs longer than kRevShortRun listed for k_rev_long_runs
+    uint32_t sb_shift;                  // K2, bucket sort: super-bucket = bucket >> sb_shift
     uint32_t tile_ticket[kMaxDigits];   // K3
     int32_t digit_of_slot[kMaxDigits];  // K2
     int32_t src_of_slot[kMaxDigits];
@@ -93,6 +94,7 @@ struct RadixDigitizer {
         for (int p = 0; p < kDigits; ++p) d[p] = digit_sh(key, 8u * p);
     }
     __device__ __forceinline__ bool in_range(K) const { return true; }
+    void plan_args(int*, int*, uint32_t*, uint32_t*, uint32_t*) const {}  // K2 needs nothing more
 };
 
 // ------------------------------------------------------------------- K1
@@ -246,12 +248,23 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
 // One CTA of kRadix threads.  flags: kPlanSkipSorted (a sorted input needs no
 // pass), kPlanKeepTrivial (run every digit pass, even one-digit ones: a scatter
 // pass must move the keys).
-constexpr int kPlanSkipSorted = 1, kPlanKeepTrivial = 2, kPlanCounting = 4;
+// kPlanAdaptiveLow (bucket sort): digit 0 is the optional fine pass -- it runs only
+// when the top digit's histogram shows skew (a bin above kSkewFactor times the
+// mean), and sb_shift follows (sb_fine with it, sb_coarse without).
+constexpr int kPlanSkipSorted = 1, kPlanKeepTrivial = 2, kPlanCounting = 4, kPlanAdaptiveLow = 8;
+constexpr uint64_t kSkewFactor = 4;
 template <int D>
-__global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, uint64_t n, int flags) {
+__global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, uint64_t n, int flags, int top_digit = 0,
+                                                 uint32_t top_bins = kRadix, uint32_t sb_fine = 0,
+                                                 uint32_t sb_coarse = 0) {
     __shared__ uint32_t warp_tot[kRadix / 32];
     __shared__ int trivial[kMaxDigits];
     const int t = threadIdx.x;
+    // skew: a bin of the top digit holds more than kSkewFactor times its share under
+    // uniform keys (top_bins = the bins the bucket range can reach)
+    const int skewed = (flags & kPlanAdaptiveLow)
+                           ? __syncthreads_or(static_cast<uint64_t>(st->hist[top_digit][t]) * top_bins > kSkewFactor * n)
+                           : 0;
     for (int p = 0; p < D; ++p) {
         const uint32_t v = st->hist[p][t];
         const uint32_t inc = warp_inclusive_scan(v);
@@ -260,9 +273,10 @@ __global__ void __launch_bounds__(kRadix) k_plan(RadixState* __restrict__ st, ui
         uint32_t pre = 0;
         for (int w = 0; w < t / 32; ++w) pre += warp_tot[w];
         st->offs[p][t] = pre + inc - v;
-        if (t == 0) trivial[p] = any_full;
+        if (t == 0) trivial[p] = any_full || (p == 0 && (flags & kPlanAdaptiveLow) && !skewed);
         __syncthreads();
     }
+    if (t == 0) st->sb_shift = skewed ? sb_fine : sb_coarse;
     if (t == 0) {
         const bool sorted = (flags & kPlanSkipSorted) && st->descents == 0;
         // non-increasing input: the stable sort is the reversal with each run of

@@ -730,3 +730,41 @@ def test_graph_replay_on_caller_stream(cuda, oracle, algorithm):
         st.synchronize()
         assert np.array_equal(ko.cpu().numpy().view(np.uint32), want_k)
         assert np.array_equal(vo.cpu().numpy().view(np.uint32), want_i)
+
+
+def _bucket_passes_executed(keys_np, vals="iota"):
+    """Sort on the device with the per-phase profile on; returns (keys, positions,
+    number of executed digit passes reported by the plan)."""
+    import ctypes
+
+    import torch
+
+    from paper_1206_3511_b200 import _lib, device
+
+    lib = _lib.load()
+    t = torch.from_numpy(keys_np.view(np.int32)).cuda()
+    s = device.Sorter(keys_np.size, 4, "bucket", vals, range_bound=U32_MAX)
+    torch.cuda.synchronize()
+    lib.isort_profile_begin()
+    k, v = s(t)
+    torch.cuda.synchronize()
+    ms = (ctypes.c_float * 256)()
+    names = ctypes.create_string_buffer(256 * 16)
+    cnt, na = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.check(lib.isort_profile_end(ms, names, 16, 256, ctypes.byref(cnt), ctypes.byref(na)))
+    return k.cpu().numpy().view(np.uint32), (v.cpu().numpy().view(np.uint32) if v is not None else None), na.value
+
+
+@pytest.mark.parametrize("n", [5_000_011, 20_000_003])
+def test_bucket_adaptive_fine_pass_on_skew(cuda, oracle, n):
+    """Skewed keys (a dense normal cluster) make K2 run the optional fine bucket
+    pass (super-buckets 256x smaller) instead of sending the cluster to the radix
+    fallback; uniform keys keep the coarse plan.  Both bit-exact."""
+    rng = np.random.default_rng(n)
+    skew = np.clip(np.rint(2.0**31 + 2.0**22 * rng.standard_normal(n)), 0, U32_MAX).astype(np.uint32)
+    uni = oracle.uniform_u32(n, 5)
+    for keys, want_passes in ((skew, 3), (uni, 2)):
+        want_k, want_i = oracle.sort_u32(keys, with_index=True)
+        got_k, got_i, passes = _bucket_passes_executed(keys)
+        assert np.array_equal(got_k, want_k) and np.array_equal(got_i, want_i)
+        assert passes == want_passes, (n, passes)
