@@ -264,6 +264,12 @@ struct BucketDigitizer {
             return bucket_of<MODE>(bi, static_cast<uint64_t>(key));
         }
     }
+    // key - base: one 32-bit subtraction for u32 keys (base < 2^32 there; an
+    // out-of-range key wraps, and its meaningless digit is never used)
+    __device__ __forceinline__ uint64_t rel(K key) const {
+        if constexpr (sizeof(K) == 4) return static_cast<uint32_t>(key) - static_cast<uint32_t>(bi.base);
+        return static_cast<uint64_t>(key) - bi.base;
+    }
     __device__ __forceinline__ uint32_t shift_for(int pos) const {
         const uint32_t* t = MODE == kPow2Narrow ? tsh : shift;
         return pos == 0 ? t[0] : (pos == 1 ? t[1] : t[2]);
@@ -272,8 +278,7 @@ struct BucketDigitizer {
     // call is failing with a range error; their digits are then meaningless but < 256.
     __device__ __forceinline__ uint32_t digit_sh(K key, uint32_t sh) const {
         if (MODE == kPow2Narrow) {  // floor(n * k / 2^s) >> shift = (n * k) >> (s + shift); n, k < 2^32
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) *
-                               (static_cast<uint64_t>(key) - bi.base);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
             return sh < 64 ? static_cast<uint32_t>(p >> sh) & (kRadix - 1) : 0u;
         }
         return static_cast<uint32_t>(bidx(key) >> sh) & (kRadix - 1);
@@ -281,8 +286,7 @@ struct BucketDigitizer {
     __device__ __forceinline__ uint32_t digit(K key, int pos) const { return digit_sh(key, shift_for(pos)); }
     __device__ __forceinline__ void all_digits(K key, uint32_t (&d)[kDigits]) const {
         if (MODE == kPow2Narrow) {
-            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) *
-                               (static_cast<uint64_t>(key) - bi.base);
+            const uint64_t p = static_cast<uint64_t>(static_cast<uint32_t>(bi.count)) * rel(key);
 #pragma unroll
             for (int q = 0; q < kDigits; ++q) d[q] = static_cast<uint32_t>(p >> tshc[q]) & dmask[q];
             return;

@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(BLOCK) k_upfront(const K* __restrict__ keys, u
             // flight per thread); the successor key for the sortedness check comes
             // from the next lane, or the next block's lane 0.
             const uint32_t nv = n32 / V;
-            constexpr int U = ISORT_UF_UNROLL;
+            // loads in flight per thread: 8 for radix digits, 4 for bucket digits (more
+            // registers per key; A/B on B200: 0.105 vs 0.110 ms at 10^8)
+            constexpr int U = Dz::kCheapDigit && sizeof(K) == 4 && D == 4 ? ISORT_UF_UNROLL : 4;
             const uint32_t wstride = gridDim.x * (BLOCK / 32) * 32 * U;
             // successor of the last whole 4-key group: the scalar tail's first key, or none
             const K tail_next = nv * V < n32 ? keys[nv * V] : static_cast<K>(~static_cast<K>(0));

@@ -1,5 +1,6 @@
 """A/B of libisort builds by phase: per-kernel CUDA-event times (isort_profile_*)
-of the radix sort of 1e8 seeded u32 keys, averaged over reps.
+of the radix sort (AB_ALG=bucket: the bucket sort) of 1e8 seeded u32 keys,
+averaged over reps.
     python tools/ab_phases.py LIB.so [LIB.so ...]"""
 import ctypes
 import os
@@ -21,15 +22,24 @@ for so in sys.argv[1:]:
         f = getattr(lib, name, None)
         if f is not None:
             f.restype, f.argtypes = res, args
-    tb = lib.isort_radix_temp_bytes(n, 4, 0)
+    bucket = os.environ.get("AB_ALG") == "bucket"
+    tb = (lib.isort_bucket_temp_bytes if bucket else lib.isort_radix_temp_bytes)(n, 4, 0)
     temp = torch.empty(tb, dtype=torch.uint8, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        if bucket:
+            lib.isort_bucket_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, (1 << 32) - 1, 0,
+                                      temp.data_ptr(), tb, s)
+        else:
+            lib.isort_radix_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, 0, temp.data_ptr(), tb, s)
+
     for _ in range(3):
-        lib.isort_radix_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, 0, temp.data_ptr(), tb, s)
+        run()
     torch.cuda.synchronize()
     lib.isort_profile_begin()
     for _ in range(reps):
-        lib.isort_radix_sort_u32(keys.data_ptr(), out.data_ptr(), None, None, n, 0, temp.data_ptr(), tb, s)
+        run()
     torch.cuda.synchronize()
     ms = (ctypes.c_float * 4096)()
     names = ctypes.create_string_buffer(4096 * 16)
