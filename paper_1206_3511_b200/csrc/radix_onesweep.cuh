@@ -461,6 +461,27 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef ISORT_SKELETON
+#define ISORT_SKELETON 0  // bit 0: key loads hashed, bit 1: key stores sunk
+#endif
+// Measurement builds only ("skeleton"): the one-sweep pass
+// with its key loads replaced by a hash of the address (the same key for the
+// same address, so counts and ranks agree) and/or its key stores by a register
+// sink -- what the pass costs without its HBM traffic.  Output is not sorted.
+__device__ __forceinline__ uint32_t skel_key(const void* p) {
+    uint32_t x = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) * 0x9E3779B1u;
+    x ^= x >> 15;
+    x *= 0x85EBCA6Bu;
+    return x ^ (x >> 13);
+}
+#if ISORT_SKELETON & 1
+__device__ __forceinline__ uint4 ldg_v4_hint(const uint4* p, uint64_t) {
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+    return make_uint4(skel_key(q), skel_key(q + 1), skel_key(q + 2), skel_key(q + 3));
+}
+__device__ __forceinline__ uint32_t ldg_hint(const uint32_t* p, uint64_t) { return skel_key(p); }
+__device__ __forceinline__ uint64_t ldg_hint(const uint64_t* p, uint64_t) { return skel_key(p); }
+#else
 __device__ __forceinline__ uint4 ldg_v4_hint(const uint4* p, uint64_t pol) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -478,12 +499,18 @@ __device__ __forceinline__ uint64_t ldg_hint(const uint64_t* p, uint64_t pol) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
     return v;
 }
+#endif
+#if ISORT_SKELETON & 2
+__device__ __forceinline__ void stg_hint(uint32_t* p, uint32_t v, uint64_t) { asm volatile("" ::"l"(p), "r"(v)); }
+__device__ __forceinline__ void stg_hint(uint64_t* p, uint64_t v, uint64_t) { asm volatile("" ::"l"(p), "l"(v)); }
+#else
 __device__ __forceinline__ void stg_hint(uint32_t* p, uint32_t v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void stg_hint(uint64_t* p, uint64_t v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
+#endif
 
 // Stable slot of a key: slot = atomicAdd(counter), relying on lane-ordered
 // same-address shared atomics; SAFE: __match_any_sync peers instead.
