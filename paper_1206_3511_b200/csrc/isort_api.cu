@@ -1013,7 +1013,8 @@ int partition_scatter_device(const K* kin, const uint32_t* vin, uint64_t n, cons
     const bool iota = vmode == ISORT_VALS_IOTA;
     // the layout is the payload one (it covers both); the tile count must match the
     // pass configuration actually launched (keys-only tiles are twice as long)
-    const uint32_t tiles = radix_layout<K>(n, vals).tiles;
+    const int stile = vals ? scatter_tile<K, true>(n) : scatter_tile<K, false>(n);
+    const uint32_t tiles = static_cast<uint32_t>((n + stile - 1) / stile);
     if (n < kSmallN) {
         if (vals)
             launch_passes<K, true, DestDigitizer<K>, PassCfg<K, true, 1>, true>(kin, nullptr, nullptr, vin, nullptr,

@@ -14,6 +14,7 @@
 #include "isort_common.cuh"
 #include "isort_internal.h"
 #include "radix_onesweep.cuh"
+#include "radix_onesweep_tma.cuh"
 
 namespace isort {
 
@@ -73,8 +74,35 @@ struct PassCfg {
     static constexpr int kCtasPerSm = ISORT_PASS_MINB_OF(kBlock);
 };
 
+// Keys-only u32 passes over large inputs take the bulk-copy write-out kernel
+// (k_onesweep_t, radix_onesweep_tma.cuh): one chunk of kIpt keys per thread.
+#ifndef ISORT_PASS_TMA
+#define ISORT_PASS_TMA 1
+#endif
+#ifndef ISORT_PASS_IPT_T
+#define ISORT_PASS_IPT_T 32
+#endif
+template <typename K>
+struct PassCfgT {
+    static constexpr int kBlock = 512;
+    static constexpr int kIpt = ISORT_PASS_IPT_T;
+    static constexpr int kTile = kBlock * kIpt;
+    static constexpr int kCtasPerSm = 1024 / kBlock;
+};
+template <typename K, bool VALS>
+constexpr bool pass_uses_tma() {
+    return ISORT_PASS_TMA && !VALS && sizeof(K) == 4;
+}
+
+// Tile of the pipeline's digit passes (launch_radix_pipeline) over n keys.
 template <typename K, bool VALS>
 inline int pass_tile(uint64_t n) {
+    if (n < kSmallN) return PassCfg<K, VALS, 1>::kTile;
+    return pass_uses_tma<K, VALS>() ? PassCfgT<K>::kTile : PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
+}
+// Tile of the partition (scatter) pass, which keeps the k_onesweep shapes.
+template <typename K, bool VALS>
+inline int scatter_tile(uint64_t n) {
     return n < kSmallN ? PassCfg<K, VALS, 1>::kTile : PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
 }
 
@@ -125,6 +153,9 @@ void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t
                    uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
                    const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{});
 template <typename K, typename Dz>
+void launch_passes_t(const K* kin, K* kout, K* kalt, uint64_t n, RadixState* st, void* lookback, uint32_t tiles,
+                     const Dz& dz, cudaStream_t s);
+template <typename K, typename Dz>
 int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz,
                      int plan_flags, bool zero_state, cudaStream_t s);
 template <typename K, bool VALS, typename Dz>
@@ -157,6 +188,30 @@ void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t
     for (int slot = 0; slot < D; ++slot) {
         kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
                                                         tiles, slot, dz, scat);
+        static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
+                                                     "pass4", "pass5", "pass6", "pass7"};
+        prof_mark(s, kPassNames[slot]);
+    }
+}
+
+// Keys-only passes with the bulk-copy write-out (k_onesweep_t), one launch per digit slot.
+template <typename K, typename Dz>
+void launch_passes_t(const K* kin, K* kout, K* kalt, uint64_t n, RadixState* st, void* lookback, uint32_t tiles,
+                     const Dz& dz, cudaStream_t s) {
+    constexpr int D = Dz::kDigits;
+    using Cfg = PassCfgT<K>;
+    using Smem = OnesweepTSmem<K, Cfg::kBlock, Cfg::kIpt>;
+    const bool fast = rank_fast_path_ok();
+    const bool narrow = lb_word_bytes(n) == 4;
+    auto* kern = fast ? (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, false, uint32_t>
+                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, false, unsigned long long>)
+                      : (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, true, uint32_t>
+                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, true, unsigned long long>);
+    set_max_smem_once(kern, sizeof(Smem));
+    const unsigned cap = static_cast<unsigned>(Cfg::kCtasPerSm * sm_count());
+    const unsigned grid3 = tiles < cap ? tiles : cap;
+    for (int slot = 0; slot < D; ++slot) {
+        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, n, st, lookback, tiles, slot, dz);
         static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
                                                      "pass4", "pass5", "pass6", "pass7"};
         prof_mark(s, kPassNames[slot]);
@@ -212,6 +267,8 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     if (n < kSmallN)
         launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
                                                         dz, s);
+    else if constexpr (pass_uses_tma<K, VALS>())
+        launch_passes_t<K, Dz>(kin, kout, kalt, n, st, lookback, tiles, dz, s);
     else
         launch_passes<K, VALS, Dz, PassCfg<K, VALS, ISORT_PASS_CHUNKS>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
                                                         dz, s);

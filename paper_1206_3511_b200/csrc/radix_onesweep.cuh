@@ -461,8 +461,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef ISORT_EARLY_TICKET
+#define ISORT_EARLY_TICKET 0
+#endif
+#ifndef ISORT_PREFETCH
+#define ISORT_PREFETCH 0
+#endif
+constexpr int kPrefetchParts = 16;  // threads that each ask 1/16 of the next tile into L2
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 #ifndef ISORT_SKELETON
-#define ISORT_SKELETON 0  // bit 0: key loads hashed, bit 1: key stores sunk
+#define ISORT_SKELETON 0  // bit 0: key loads hashed, bit 1: key stores sunk, bit 2: stores linear
+#endif
+#ifndef ISORT_SKEL_SHIFT
+#define ISORT_SKEL_SHIFT 0  // bit 2: staged slot j goes to tile position j + this (store alignment probe)
 #endif
 // Measurement builds only ("skeleton"): the one-sweep pass
 // with its key loads replaced by a hash of the address (the same key for the
@@ -778,9 +791,14 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
 #endif
 
     bool hot_prev = false;  // phase 1 guesses from this CTA's previous tile
+#if ISORT_EARLY_TICKET
+    if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
+#endif
     for (;;) {
         ISORT_TICK(q0);
+#if !ISORT_EARLY_TICKET
         if (tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
+#endif
         {
             uint4* c4 = reinterpret_cast<uint4*>(&sm.cnt[0][0][0]);
             for (int i = tid; i < NCHUNK * kWarps * kRadix / 4; i += BLOCK) c4[i] = make_uint4(0, 0, 0, 0);
@@ -855,6 +873,9 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
                     sm.run_start[ISORT_PASS_BULK ? c : 0][d] = base;
                 }
                 sm.out_base[c][d] = run - base;
+#if ISORT_SKELETON & 4
+                sm.out_base[c][d] = static_cast<uint32_t>(tile_base) + c * kChunk + (tile + 1 < num_tiles ? ISORT_SKEL_SHIFT : 0);
+#endif
                 run += cc[c];
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) {  // per-warp slot bases for phase 2
@@ -906,8 +927,15 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
 #endif
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + tid], LT::kInc | (excl + late_tot));
 #pragma unroll
-                for (int cc = 0; cc < NCHUNK; ++cc) sm.out_base[cc][tid] += excl;
+                for (int cc = 0; cc < NCHUNK; ++cc) sm.out_base[cc][tid] += (ISORT_SKELETON & 4) ? 0u : excl;
             }
+#if ISORT_EARLY_TICKET || ISORT_PREFETCH
+            // The next tile's ticket is taken before this tile's last write-out, and its
+            // keys are asked into L2 while the write-out runs (the count phase then
+            // starts on L2 hits).  The owner of a ticket is a running CTA, as before.
+            const bool last_chunk = c + 1 == NCHUNK || c0 + kChunk >= tile_len;
+            if (ISORT_EARLY_TICKET && last_chunk && tid == 0) sm.tile_id = atomicAdd(&st->tile_ticket[slot], 1u);
+#endif
             if constexpr (kBulkWrite) {
                 fence_proxy_async_smem();  // the staging stores, visible to the bulk copies
                 __syncthreads();
@@ -915,7 +943,33 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_MINB_OF(BLOCK))
                 __syncthreads();
                 continue;
             }
+#if ISORT_SKELETON & 8  // store-path probe: the staged chunk leaves by one linear bulk copy
+            fence_proxy_async_smem();
             __syncthreads();
+            if (tid == 0) {
+                bulk_s2g(dst + tile_base + c0, sm.keys, (valid * static_cast<uint32_t>(sizeof(K))) & ~15u);
+                bulk_wait_read();
+            }
+            __syncthreads();
+            continue;
+#endif
+            __syncthreads();
+#if ISORT_EARLY_TICKET || ISORT_PREFETCH
+            if (ISORT_PREFETCH && last_chunk && vec && tid < kPrefetchParts) {
+                const uint32_t nt = ISORT_EARLY_TICKET ? sm.tile_id : tile + gridDim.x;  // exact / the likely next
+                const uint64_t nb = static_cast<uint64_t>(nt) * kTile;
+                if (nt < num_tiles && nb < n) {
+                    constexpr uint32_t kPart = kTile / kPrefetchParts;  // keys per prefetching thread
+                    const uint64_t b = nb + static_cast<uint64_t>(tid) * kPart;
+                    if (b < n) {
+                        const uint64_t left = n - b;
+                        const uint32_t cnt = left < kPart ? static_cast<uint32_t>(left) : kPart;
+                        const uint32_t bytes = (cnt * static_cast<uint32_t>(sizeof(K))) & ~15u;
+                        if (bytes) bulk_prefetch_l2(src + b, bytes);
+                    }
+                }
+            }
+#endif
             if (full)
                 chunk_write<true, SCATTER, K, Dz, BLOCK, IPT, VALS>(sm, c, dst, vdst, valid, dsh, dz, pol_stream,
                                                                     s_kbase, s_vbase);

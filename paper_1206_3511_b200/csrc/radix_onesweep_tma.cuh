@@ -1,0 +1,252 @@
+// radix_onesweep_tma.cuh -- the one-sweep digit pass with a bulk-copy (TMA)
+// write-out: keys-only passes over large inputs (K3t).
+//
+// Same contract as k_onesweep (radix_onesweep.cuh): one stable counting pass of
+// the LSD sort (sort.cpp:77-110) over tiles taken by atomic ticket, global
+// offsets by decoupled look-back.  What differs is the shape of a tile:
+//   * one chunk per tile, read ONCE: the tile's keys stay in registers between
+//     the count and the rank (warp-striped, so (item, lane) order is input order);
+//   * every digit's run is staged at a slot congruent to its global position
+//     modulo one 16-byte block, so the run's aligned interior leaves shared memory
+//     by one cp.async.bulk (TMA store) issued by the digit's thread; only the
+//     <= 3 + 3 keys around it are plain stores.  The copy engine reads the staged
+//     run while the CTA already counts its next tile: nothing waits for it until
+//     the next tile's rank, which is a whole count phase later;
+//   * the next tile's ticket is taken during the per-digit section and its keys
+//     are loaded into the registers the rank has just consumed.
+// Against k_onesweep this removes, per 32 keys, the second key read (1 L1
+// wavefront), the staged-key load (1), the out_base lookup (~1.5) and the
+// scattered STG (~2.5) of the write-out, for ~1.5-2 wavefronts of run-edge
+// stores.
+#pragma once
+
+#include "radix_onesweep.cuh"
+
+namespace isort {
+
+template <typename K, int BLOCK, int IPT>
+struct OnesweepTSmem {
+    static constexpr int kWarps = BLOCK / 32;
+    static constexpr int kTile = BLOCK * IPT;
+    static constexpr int kVec = 16 / static_cast<int>(sizeof(K));  // keys per 16-byte block
+    static constexpr int kStage = kTile + kVec * kRadix;           // <= kVec - 1 pad slots before each run (+ 1 spare)
+    uint32_t cnt[kWarps][kRadix];  // counts; then per-warp slot bases
+    uint32_t offs[kRadix];         // pass digit offsets (from K2)
+    uint32_t tot_w[kRadix / 32];
+    uint32_t run_slot[kRadix];     // digit d's run: first staging slot,
+    uint32_t run_len[kRadix];      // keys,
+    uint32_t run_g[kRadix];        // and global index of its first key
+    uint32_t tile_next;
+    alignas(16) K keys[kStage];
+};
+
+#ifndef ISORT_T_LB_WINDOW
+#define ISORT_T_LB_WINDOW 8  // the tile's keys are live in registers during the walk: a narrower window than K3's
+#endif
+constexpr int kLookbackWindowT = ISORT_T_LB_WINDOW;
+
+template <typename K, typename Dz, int BLOCK, int IPT, bool SAFE, typename LW>
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+    k_onesweep_t(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt, uint64_t n,
+                 RadixState* __restrict__ st, void* __restrict__ lookback, uint32_t num_tiles, int slot, Dz dz) {
+    using LT = LbTraits<LW>;
+    using Smem = OnesweepTSmem<K, BLOCK, IPT>;
+    constexpr int kWarps = Smem::kWarps;
+    constexpr int kTile = Smem::kTile;
+    constexpr uint32_t kVec = Smem::kVec;
+    static_assert(BLOCK >= 2 * kRadix && BLOCK % 32 == 0, "threads [0, kRadix) own a digit, the next kRadix its run edges");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+
+    if (slot >= static_cast<int>(st->n_active)) return;  // trivial / skipped pass
+    const int pos = st->digit_of_slot[slot];
+    const int src_id = st->src_of_slot[slot];
+    const int dst_id = st->dst_of_slot[slot];
+    const K* src = src_id == kBufIn ? keys_in : (src_id == kBufOut ? keys_out : keys_alt);
+    K* dst = dst_id == kBufOut ? keys_out : keys_alt;
+    const uint32_t dsh = dz.shift_for(pos);
+    LW* lb = static_cast<LW*>(lookback) + static_cast<size_t>(slot) * num_tiles * kRadix;
+    // key index of dst[0] within its 16-byte block: staged slot == global index + mis (mod kVec)
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) / sizeof(K)) & (kVec - 1);
+    const uint64_t pol = ISORT_POL_STREAM;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t wofs = static_cast<uint32_t>(warp) * 32u * IPT + lane;
+    uint32_t* const wc = sm.cnt[warp];
+    if (tid < kRadix) sm.offs[tid] = st->offs[pos][tid];
+    if (tid == 0) sm.tile_next = atomicAdd(&st->tile_ticket[slot], 1u);
+    {
+        uint4* c4 = reinterpret_cast<uint4*>(&sm.cnt[0][0]);
+        for (int i = tid; i < kWarps * kRadix / 4; i += BLOCK) c4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+
+    auto len_of = [&](uint32_t t) -> uint32_t {
+        if (t >= num_tiles) return 0u;
+        const uint64_t b = static_cast<uint64_t>(t) * kTile;
+        if (b >= n) return 0u;
+        return n - b < static_cast<uint64_t>(kTile) ? static_cast<uint32_t>(n - b) : static_cast<uint32_t>(kTile);
+    };
+    uint32_t tile = sm.tile_next;
+    uint32_t tile_len = len_of(tile);
+    K key[IPT];
+    {
+        const K* ws = src + static_cast<uint64_t>(tile) * kTile + wofs;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) key[i] = wofs + i * 32u < tile_len ? ldg_hint(ws + i * 32, pol) : static_cast<K>(0);
+    }
+
+#ifdef ISORT_PHASE_TIMING
+    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0, qa = 0, qb = 0, qc = 0;
+#define ISORT_TTICK(v) \
+    if (tid == 0) v = clock64()
+#else
+#define ISORT_TTICK(v)
+#endif
+    bool hot_prev = false;  // the count guesses from this CTA's previous tile
+    while (tile_len != 0) {
+        ISORT_TTICK(q0);
+        const bool full = tile_len == static_cast<uint32_t>(kTile);
+        // ---------------- count: per-warp digit counts of the keys in registers
+        if (full && hot_prev) {
+            bool agg = true;
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) count_digit_t<true>(wc, dz.digit_sh(key[i], dsh), agg);
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i)
+                if (full || wofs + i * 32u < tile_len) atomicAdd(&wc[dz.digit_sh(key[i], dsh)], 1u);
+        }
+        __syncthreads();
+        ISORT_TTICK(q1);
+
+        // ---------------- one thread per digit: total, look-back, aligned run start, slot bases
+        int nonzero = 0;
+        if (tid < kRadix) {
+            ISORT_TTICK(qa);
+            bulk_wait_read();  // the previous tile's copies have read the staging buffer
+            ISORT_TTICK(qb);
+            const int d = tid;
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) tot += sm.cnt[w][d];
+            nonzero = tot != 0;
+            uint32_t excl = 0;
+            if (tile == 0) {
+                st_relaxed_gpu(&lb[d], LT::kInc | tot);
+            } else {
+                st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kAgg | tot);
+                excl = lookback_digit<LW, kLookbackWindowT>(lb, static_cast<int>(tile) - 1, d, 0u);
+                st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kInc | (excl + tot));
+            }
+            ISORT_TTICK(qc);
+            const uint32_t sc = warp_inclusive_scan(tot);
+            if (lane == 31) sm.tot_w[warp] = sc;
+            if (BLOCK == kRadix)
+                __syncthreads();
+            else
+                asm volatile("bar.sync 1, %0;" ::"n"(kRadix));
+            uint32_t pre = 0;
+#pragma unroll
+            for (int w = 0; w < kRadix / 32; ++w) pre += w < warp ? sm.tot_w[w] : 0u;
+            const uint32_t run_g = sm.offs[d] + excl;
+            uint32_t base = pre + sc - tot + kVec * static_cast<uint32_t>(d);
+            base += (run_g + mis - base) & (kVec - 1);  // slot == global index + mis (mod kVec)
+            sm.run_slot[d] = base;
+            sm.run_len[d] = tot;
+            sm.run_g[d] = run_g;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {  // per-warp slot bases for the rank
+                const uint32_t v = sm.cnt[w][d];
+                sm.cnt[w][d] = base;
+                base += v;
+            }
+        }
+        const bool hot = __syncthreads_count(nonzero) <= kHotDigits;
+        hot_prev = hot;
+        ISORT_TTICK(q2);
+
+        // ---------------- rank and stage
+        if (full && hot) {
+            bool agg = true;
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const uint32_t s = warp_slot_agg<SAFE>(wc, dz.digit_sh(key[i], dsh), agg);
+                sm.keys[s] = key[i];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                if (full || wofs + i * 32u < tile_len) {
+                    const uint32_t s = warp_slot<SAFE>(wc, dz.digit_sh(key[i], dsh));
+                    sm.keys[s] = key[i];
+                }
+            }
+        }
+        // the next ticket is taken late, as in K3: a tile's aggregate follows its ticket by
+        // one count phase, so the look-back of the tiles behind it finds it published
+        if (tid == 0) sm.tile_next = atomicAdd(&st->tile_ticket[slot], 1u);
+        __syncwarp();
+        {  // this warp's counters are done: zero them for its next count (no other warp reads them before)
+            uint4* r = reinterpret_cast<uint4*>(wc);
+#pragma unroll
+            for (int q = 0; q < kRadix / 4 / 32; ++q) r[lane + 32 * q] = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();  // the staging stores, visible to the bulk copies
+        __syncthreads();
+        ISORT_TTICK(q3);
+        const uint32_t next = sm.tile_next;
+        const uint32_t next_len = len_of(next);
+        {  // the next tile's keys are in flight during the write-out
+            const K* ns = src + static_cast<uint64_t>(next < num_tiles ? next : 0u) * kTile + wofs;
+#pragma unroll
+            for (int i = 0; i < IPT; ++i)
+                key[i] = wofs + i * 32u < next_len ? ldg_hint(ns + i * 32, pol) : static_cast<K>(0);
+        }
+
+        // ---------------- write-out of digit d's run -> dst[run_g, run_g + run_len): threads
+        // [0, kRadix) issue the bulk copy of its aligned interior, threads [kRadix, 2 kRadix)
+        // store the keys around it
+        {
+            const int d = tid & (kRadix - 1);
+            const uint32_t run_len = sm.run_len[d];
+            if (run_len != 0 && tid < 2 * kRadix) {
+                const uint32_t run_g = sm.run_g[d];
+                const K* sp = sm.keys + sm.run_slot[d];
+                K* gp = dst + run_g;
+                uint32_t head = (kVec - ((run_g + mis) & (kVec - 1))) & (kVec - 1);
+                head = head < run_len ? head : run_len;
+                const uint32_t body = (run_len - head) & ~(kVec - 1);
+                if (tid < kRadix) {
+                    if (body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
+                } else {
+                    for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
+                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+                }
+            }
+        }
+        tile = next;
+        tile_len = next_len;
+        ISORT_TTICK(q4);
+#ifdef ISORT_PHASE_TIMING
+        acc[0] += q1 - q0;  // count
+        acc[1] += q2 - q1;  // per-digit section
+        acc[2] += q3 - q2;  // rank + next loads
+        acc[3] += 1;
+        acc[4] += q4 - q3;  // write-out (thread 0's run)
+        acc[5] += qb - qa;  // wait for the previous copies
+        acc[6] += qc - qb;  // totals + look-back
+#endif
+    }
+#ifdef ISORT_PHASE_TIMING
+    if (tid == 0)
+        for (int i = 0; i < 7; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
+#endif
+#undef ISORT_TTICK
+    if (tid < kRadix) bulk_wait_all();  // this CTA's bulk stores complete before it exits
+}
+
+}  // namespace isort

@@ -12,7 +12,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 so = os.path.join(ROOT, "tools", "libisort_timing.so")
-if not os.path.exists(so) or "--rebuild" in sys.argv:
+libs = [a for a in sys.argv[1:] if a.endswith(".so")]  # a -DISORT_PHASE_TIMING build made by tools/build_variant.py
+if libs:
+    so = os.path.abspath(libs[0])
+elif not os.path.exists(so) or "--rebuild" in sys.argv:
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                     "-DISORT_PHASE_TIMING", "-Xcompiler", "-fPIC", "-shared", "-o", so,
                     *sorted(glob.glob(os.path.join(ROOT, "paper_1206_3511_b200", "csrc", "*.cu")))], check=True)
@@ -44,7 +47,8 @@ import ctypes as C
 class RadixState(C.Structure):
     _fields_ = [("hist", C.c_uint32 * 2048), ("offs", C.c_uint32 * 2048), ("max_key", C.c_uint64),
                 ("first_bad", C.c_uint64), ("descents", C.c_uint32), ("ascents", C.c_uint32),
-                ("n_active", C.c_uint32), ("copy_in_to_out", C.c_uint32), ("reversed", C.c_uint32), ("tile_ticket", C.c_uint32 * 8),
+                ("n_active", C.c_uint32), ("copy_in_to_out", C.c_uint32), ("reversed", C.c_uint32), ("counting", C.c_uint32),
+                ("rev_long", C.c_uint32), ("sb_shift", C.c_uint32), ("tile_ticket", C.c_uint32 * 8),
                 ("digit_of_slot", C.c_int32 * 8), ("src_of_slot", C.c_int32 * 8), ("dst_of_slot", C.c_int32 * 8),
                 ("prof", C.c_uint64 * 16)]
 
@@ -54,3 +58,7 @@ acc = temp[off:off + 128].cpu().numpy().view(np.uint64)
 tiles = int(acc[3])
 print(f"tiles={tiles}  cycles/tile: phase1={acc[0] / tiles:.0f}  totals+lookback={acc[1] / tiles:.0f}"
       f"  bases+phase2={acc[2] / tiles:.0f}")
+# k_onesweep_t (radix_onesweep_tma.cuh): count, per-digit section, rank, write-out; inside the section: copy wait, totals + look-back
+print("k_onesweep_t cycles/tile: " + "  ".join(
+    f"{name}={acc[i] / tiles:.0f}" for name, i in (("count", 0), ("digit_section", 1), ("rank", 2), ("write_out", 4),
+                                                   ("copy_wait", 5), ("totals_lookback", 6))))
