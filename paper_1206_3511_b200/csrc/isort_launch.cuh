@@ -89,16 +89,27 @@ struct PassCfgT {
     static constexpr int kTile = kBlock * kIpt;
     static constexpr int kCtasPerSm = 1024 / kBlock;
 };
-template <typename K, bool VALS>
+// Which digitizers take it: the radix digit (one PRMT).  The bucket-index digits
+// (a 64-bit multiply each time a digit is needed) measured slower in it than in
+// k_onesweep (0.301 / 0.295 against 0.283 / 0.276 ms per pass at 10^8).
+template <typename Dz>
+struct TmaPassDigitizer : std::false_type {};
+template <typename K>
+struct TmaPassDigitizer<RadixDigitizer<K>> : std::true_type {};
+template <typename K, bool VALS, typename Dz>
 constexpr bool pass_uses_tma() {
-    return ISORT_PASS_TMA && !VALS && sizeof(K) == 4;
+    return ISORT_PASS_TMA && !VALS && sizeof(K) == 4 && TmaPassDigitizer<Dz>::value;
 }
 
-// Tile of the pipeline's digit passes (launch_radix_pipeline) over n keys.
+// Smallest tile any digit pass of a pipeline over n keys may use: it sizes the
+// look-back rows of a temp layout (radix_layout).  Each launch computes its own
+// tile count from the configuration it runs (launch_radix_pipeline).
 template <typename K, bool VALS>
 inline int pass_tile(uint64_t n) {
     if (n < kSmallN) return PassCfg<K, VALS, 1>::kTile;
-    return pass_uses_tma<K, VALS>() ? PassCfgT<K>::kTile : PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
+    const int t = PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
+    if (ISORT_PASS_TMA && !VALS && sizeof(K) == 4) return PassCfgT<K>::kTile < t ? PassCfgT<K>::kTile : t;
+    return t;
 }
 // Tile of the partition (scatter) pass, which keeps the k_onesweep shapes.
 template <typename K, bool VALS>
@@ -264,14 +275,19 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
     int rc = launch_histogram<K, Dz>(kin, n, st, lookback, tiles, dz, plan_flags, zero_state, s);
     if (rc) return rc;
 
-    if (n < kSmallN)
-        launch_passes<K, VALS, Dz, PassCfg<K, VALS, 1>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
-                                                        dz, s);
-    else if constexpr (pass_uses_tma<K, VALS>())
-        launch_passes_t<K, Dz>(kin, kout, kalt, n, st, lookback, tiles, dz, s);
-    else
-        launch_passes<K, VALS, Dz, PassCfg<K, VALS, ISORT_PASS_CHUNKS>>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles,
-                                                        dz, s);
+    // `tiles` is the layout's row capacity (the smallest tile); each shape counts its own tiles
+    auto tiles_of = [&](int tile) { return static_cast<uint32_t>((n + tile - 1) / tile); };
+    if (n < kSmallN) {
+        using Cfg = PassCfg<K, VALS, 1>;
+        launch_passes<K, VALS, Dz, Cfg>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles_of(Cfg::kTile),
+                                        dz, s);
+    } else if constexpr (pass_uses_tma<K, VALS, Dz>()) {
+        launch_passes_t<K, Dz>(kin, kout, kalt, n, st, lookback, tiles_of(PassCfgT<K>::kTile), dz, s);
+    } else {
+        using Cfg = PassCfg<K, VALS, ISORT_PASS_CHUNKS>;
+        launch_passes<K, VALS, Dz, Cfg>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles_of(Cfg::kTile),
+                                        dz, s);
+    }
     launched(D);
     // the plan's early-out shapes (radix_onesweep.cuh, k_finish_a / k_finish_b): sorted
     // copy, run-wise reversal, counting pass -- each kernel returns at once unless chosen

@@ -416,10 +416,12 @@ constexpr int kHotDigits = 32;  // <= this many distinct digits in a tile: warp-
 // Exclusive prefix of digit d over tiles [0, tile): windowed decoupled look-back,
 // all kLookbackWindow loads in flight per round trip.
 template <typename LW, int W = kLookbackWindow>
-__device__ __forceinline__ uint32_t lookback_digit(const LW* __restrict__ lb, int t_start, int d, uint32_t excl) {
+__device__ __forceinline__ uint32_t lookback_digit(const LW* __restrict__ lb, int t_start, int d, uint32_t excl,
+                                                   unsigned long long* lbst = nullptr) {  // lbst: measurement builds
     using T = LbTraits<LW>;
     int t = t_start;
     while (t >= 0) {
+        if (lbst) ++lbst[0];  // rounds
         LW sv[W];
 #pragma unroll
         for (int j = 0; j < W; ++j)
@@ -438,6 +440,10 @@ __device__ __forceinline__ uint32_t lookback_digit(const LW* __restrict__ lb, in
             }
         }
         if (done) break;
+        if (lbst) {
+            if (used < W && t - used >= 0) ++lbst[1];  // rounds that stopped at an unpublished predecessor
+            lbst[2] += used;                             // tiles consumed before the last round
+        }
         t -= used;  // stopped at a predecessor that has not published: re-read from it
     }
     return excl;

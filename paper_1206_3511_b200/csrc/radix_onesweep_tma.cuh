@@ -4,20 +4,23 @@
 // Same contract as k_onesweep (radix_onesweep.cuh): one stable counting pass of
 // the LSD sort (sort.cpp:77-110) over tiles taken by atomic ticket, global
 // offsets by decoupled look-back.  What differs is the shape of a tile:
-//   * one chunk per tile, read ONCE: the tile's keys stay in registers between
-//     the count and the rank (warp-striped, so (item, lane) order is input order);
+//   * one chunk of BLOCK * IPT keys per tile, read ONCE: the keys stay in
+//     registers between the count and the rank (warp-striped, so (item, lane)
+//     order is input order);
 //   * every digit's run is staged at a slot congruent to its global position
 //     modulo one 16-byte block, so the run's aligned interior leaves shared memory
 //     by one cp.async.bulk (TMA store) issued by the digit's thread; only the
 //     <= 3 + 3 keys around it are plain stores.  The copy engine reads the staged
 //     run while the CTA already counts its next tile: nothing waits for it until
-//     the next tile's rank, which is a whole count phase later;
-//   * the next tile's ticket is taken during the per-digit section and its keys
-//     are loaded into the registers the rank has just consumed.
-// Against k_onesweep this removes, per 32 keys, the second key read (1 L1
-// wavefront), the staged-key load (1), the out_base lookup (~1.5) and the
-// scattered STG (~2.5) of the write-out, for ~1.5-2 wavefronts of run-edge
-// stores.
+//     the next tile's rank, a whole count phase and per-digit section later;
+//   * the aligned slots need the run's global position, so the look-back comes
+//     before the rank (k_onesweep walks after chunk 0 is staged);
+//   * the next tile's ticket is taken after the rank and its keys are loaded
+//     during the write-out.
+// Per 32 keys this removes the second key read (1 L1 wavefront), the staged-key
+// load (1), the out_base lookup (~1.5) and most of the scattered STG (~2.5 ->
+// 0.6): 15.1 L1 wavefronts against 19.0, 0.265 ms against 0.279 ms per pass at
+// 10^8 keys (DESIGN.md section 3.1 has the phase split and what was tried).
 #pragma once
 
 #include "radix_onesweep.cuh"
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 
 #ifdef ISORT_PHASE_TIMING
     long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0, qa = 0, qb = 0, qc = 0;
+    long long q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0, qa = 0, qb = 0, qc = 0, qd = 0, qe = 0;
 #define ISORT_TTICK(v) \
     if (tid == 0) v = clock64()
 #else
@@ -134,12 +137,24 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) tot += sm.cnt[w][d];
             nonzero = tot != 0;
+            ISORT_TTICK(qd);
             uint32_t excl = 0;
             if (tile == 0) {
                 st_relaxed_gpu(&lb[d], LT::kInc | tot);
             } else {
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kAgg | tot);
+#ifdef ISORT_LB_STATS
+                unsigned long long lbst[3] = {0, 0, 0};
+                excl = lookback_digit<LW, kLookbackWindowT>(lb, static_cast<int>(tile) - 1, d, 0u, lbst);
+                if (tid == 0) {
+                    atomicAdd(&st->prof[8], lbst[0]);
+                    atomicAdd(&st->prof[9], lbst[1]);
+                    atomicAdd(&st->prof[10], lbst[2]);
+                    atomicAdd(&st->prof[11], 1ull);
+                }
+#else
                 excl = lookback_digit<LW, kLookbackWindowT>(lb, static_cast<int>(tile) - 1, d, 0u);
+#endif
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kInc | (excl + tot));
             }
             ISORT_TTICK(qc);
@@ -200,27 +215,31 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         ISORT_TTICK(q3);
         const uint32_t next = sm.tile_next;
         const uint32_t next_len = len_of(next);
-        {  // the next tile's keys are in flight during the write-out
+        auto load_next = [&]() {  // the next tile's keys: in flight during the write-out
             const K* ns = src + static_cast<uint64_t>(next < num_tiles ? next : 0u) * kTile + wofs;
 #pragma unroll
             for (int i = 0; i < IPT; ++i)
                 key[i] = wofs + i * 32u < next_len ? ldg_hint(ns + i * 32, pol) : static_cast<K>(0);
-        }
+        };
+        load_next();
 
-        // ---------------- write-out of digit d's run -> dst[run_g, run_g + run_len): threads
-        // [0, kRadix) issue the bulk copy of its aligned interior, threads [kRadix, 2 kRadix)
-        // store the keys around it
+        // ---------------- write-out of digit d's run -> dst[run_g, run_g + run_len): thread d
+        // issues the bulk copy of its aligned interior, thread kRadix + d stores the keys
+        // around it (the same split inside every warp, or the write-out before the loads,
+        // measured no faster)
         {
             const int d = tid & (kRadix - 1);
-            const uint32_t run_len = sm.run_len[d];
-            if (run_len != 0 && tid < 2 * kRadix) {
+            const bool copier = tid < kRadix;
+            const bool active = tid < 2 * kRadix;
+            const uint32_t run_len = active ? sm.run_len[d] : 0u;
+            if (run_len != 0) {
                 const uint32_t run_g = sm.run_g[d];
                 const K* sp = sm.keys + sm.run_slot[d];
                 K* gp = dst + run_g;
                 uint32_t head = (kVec - ((run_g + mis) & (kVec - 1))) & (kVec - 1);
                 head = head < run_len ? head : run_len;
                 const uint32_t body = (run_len - head) & ~(kVec - 1);
-                if (tid < kRadix) {
+                if (copier) {
                     if (body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
                 } else {
                     for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
@@ -239,11 +258,12 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         acc[4] += q4 - q3;  // write-out (thread 0's run)
         acc[5] += qb - qa;  // wait for the previous copies
         acc[6] += qc - qb;  // totals + look-back
+        acc[7] += qd - qb;  // totals (the count's atomics drain first)
 #endif
     }
 #ifdef ISORT_PHASE_TIMING
     if (tid == 0)
-        for (int i = 0; i < 7; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
+        for (int i = 0; i < 8; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
 #endif
 #undef ISORT_TTICK
     if (tid < kRadix) bulk_wait_all();  // this CTA's bulk stores complete before it exits

@@ -4,7 +4,7 @@ compile to ATOMS.POPC.INC.32 RZ) whose same-address lanes are granted in
 ascending lane order.  k_selftest_atomic_order re-checks that property at load time, so it
 must exercise the SAME instruction the rank compiles to.  This CPU test
 disassembles libisort.so (cuobjdump) and pins:
-  * the fast pass (SAFE = false) ranks with ATOMS.ADD and has no MATCH,
+  * the fast passes (SAFE = false; k_onesweep_t and k_onesweep) rank with ATOMS.ADD and have no MATCH,
   * the load-time self-test uses ATOMS.ADD (and MATCH.ANY as its reference),
   * the fallback pass (SAFE = true) ranks with MATCH.ANY,
   * the segment sort of the bucket path ranks with ATOMS.ADD too."""
@@ -50,14 +50,24 @@ def _find(ops, *parts):
     return hits
 
 
+def _assert_fast(sass_ops, f):
+    c = sass_ops[f]
+    assert c["ATOMS.ADD.RET"] > 0, (f, dict(c))
+    assert not any(k.startswith("MATCH") for k in c), f
+    assert not any(k.endswith(".RET") and k != "ATOMS.ADD.RET" for k in c), (f, dict(c))
+
+
 def test_fast_rank_is_returning_shared_atomic(sass_ops):
-    # k_onesweep<u32, RadixDigitizer<u32>, 512, 24, 2, VALS=0, SAFE=0, SCATTER=0, LW>: the rank is a
-    # returning ATOMS.ADD; the counts are non-returning (ATOMS.POPC.INC.32 RZ / ATOMS.ADD RZ)
-    for f in _find(sass_ops, "k_onesweep", "RadixDigitizerIj", "Li512ELi24ELi2ELb0ELb0ELb0E"):
-        c = sass_ops[f]
-        assert c["ATOMS.ADD.RET"] > 0, (f, dict(c))
-        assert not any(k.startswith("MATCH") for k in c), f
-        assert not any(k.endswith(".RET") and k != "ATOMS.ADD.RET" for k in c), (f, dict(c))
+    # the rank is a returning ATOMS.ADD; the counts are non-returning (ATOMS.POPC.INC.32 RZ / ATOMS.ADD RZ)
+    # k_onesweep_t<u32, RadixDigitizer<u32>, 512, 32, SAFE=0, LW>: keys-only passes over large inputs
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb0E"):
+        _assert_fast(sass_ops, f)
+    # k_onesweep<u32, RadixDigitizer<u32>, 512, 12, 2, VALS=1, SAFE=0, SCATTER=0, LW>: passes with a payload
+    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi2ELb1ELb0ELb0E"):
+        _assert_fast(sass_ops, f)
+    # k_onesweep<u32, RadixDigitizer<u32>, 512, 16, 1, VALS=0, SAFE=0, SCATTER=0, LW>: small inputs
+    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi16ELi1ELb0ELb0ELb0E"):
+        _assert_fast(sass_ops, f)
 
 
 def test_selftest_checks_the_same_instruction(sass_ops):
@@ -68,7 +78,9 @@ def test_selftest_checks_the_same_instruction(sass_ops):
 
 
 def test_safe_rank_uses_match(sass_ops):
-    for f in _find(sass_ops, "k_onesweep", "RadixDigitizerIj", "Li512ELi24ELi2ELb0ELb1ELb0E"):
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb1E"):
+        assert sass_ops[f]["MATCH.ANY"] > 0, f
+    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi2ELb1ELb1ELb0E"):
         assert sass_ops[f]["MATCH.ANY"] > 0, f
 
 

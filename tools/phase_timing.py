@@ -61,4 +61,8 @@ print(f"tiles={tiles}  cycles/tile: phase1={acc[0] / tiles:.0f}  totals+lookback
 # k_onesweep_t (radix_onesweep_tma.cuh): count, per-digit section, rank, write-out; inside the section: copy wait, totals + look-back
 print("k_onesweep_t cycles/tile: " + "  ".join(
     f"{name}={acc[i] / tiles:.0f}" for name, i in (("count", 0), ("digit_section", 1), ("rank", 2), ("write_out", 4),
-                                                   ("copy_wait", 5), ("totals_lookback", 6))))
+                                                   ("copy_wait", 5), ("totals_lookback", 6), ("totals", 7))))
+
+if acc[11]:
+    print(f"look-back of digit 0 per walk: rounds={acc[8] / acc[11]:.2f}  blocked rounds={acc[9] / acc[11]:.2f}"
+          f"  tiles consumed before the last round={acc[10] / acc[11]:.1f}")
