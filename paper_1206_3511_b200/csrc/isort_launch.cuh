@@ -82,9 +82,12 @@ struct PassCfg {
 #ifndef ISORT_PASS_IPT_T
 #define ISORT_PASS_IPT_T 32
 #endif
+#ifndef ISORT_PASS_BLOCK_T
+#define ISORT_PASS_BLOCK_T 512
+#endif
 template <typename K>
 struct PassCfgT {
-    static constexpr int kBlock = 512;
+    static constexpr int kBlock = ISORT_PASS_BLOCK_T;
     static constexpr int kIpt = ISORT_PASS_IPT_T;
     static constexpr int kTile = kBlock * kIpt;
     static constexpr int kCtasPerSm = 1024 / kBlock;

@@ -36,15 +36,23 @@ struct OnesweepTSmem {
     uint32_t cnt[kWarps][kRadix];  // counts; then per-warp slot bases
     uint32_t offs[kRadix];         // pass digit offsets (from K2)
     uint32_t tot_w[kRadix / 32];
-    uint32_t run_slot[kRadix];     // digit d's run: first staging slot,
-    uint32_t run_len[kRadix];      // keys,
-    uint32_t run_g[kRadix];        // and global index of its first key
+    uint32_t run_slot[2][kRadix];  // digit d's run (by tile parity): first staging slot,
+    uint32_t run_len[2][kRadix];   // keys,
+    uint32_t run_g[2][kRadix];     // and global index of its first key
     uint32_t tile_next;
     alignas(16) K keys[kStage];
 };
 
+// Look-back window (predecessors read per round trip and digit).  The walk is spent
+// waiting for the nearest predecessors to publish, not reading: at 10^8 keys it
+// takes ~8,400 of a tile's 27,400 cycles whatever the window (2 / 4 / 8 / 16 / 24:
+// 0.2623 / 0.2632 / 0.2652 / 0.274 / 0.28 ms per pass), and every round reads
+// window x 1 KB per tile from L2, so a narrow window is the cheaper one.
+#ifndef ISORT_T_LATE_WRITE
+#define ISORT_T_LATE_WRITE 1
+#endif
 #ifndef ISORT_T_LB_WINDOW
-#define ISORT_T_LB_WINDOW 8  // the tile's keys are live in registers during the walk: a narrower window than K3's
+#define ISORT_T_LB_WINDOW 4
 #endif
 constexpr int kLookbackWindowT = ISORT_T_LB_WINDOW;
 
@@ -57,7 +65,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     constexpr int kWarps = Smem::kWarps;
     constexpr int kTile = Smem::kTile;
     constexpr uint32_t kVec = Smem::kVec;
-    static_assert(BLOCK >= 2 * kRadix && BLOCK % 32 == 0, "threads [0, kRadix) own a digit, the next kRadix its run edges");
+    static_assert(BLOCK >= kRadix && BLOCK % 32 == 0, "threads [0, kRadix) own a digit");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -109,6 +117,32 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 #else
 #define ISORT_TTICK(v)
 #endif
+    // Write-out of digit d's run of the tile of parity p -> dst[run_g, run_g + run_len): thread d
+    // issues the bulk copy of its aligned interior, thread kRadix + d stores the keys
+    // around it (the same split inside every warp, or the write-out before the loads,
+    // measured no faster).
+    auto write_out = [&](int p) {
+        constexpr bool kSplit = BLOCK >= 2 * kRadix;  // else thread d does both
+        const int d = tid & (kRadix - 1);
+        const bool copier = tid < kRadix;
+        const bool active = tid < 2 * kRadix;
+        const uint32_t run_len = active ? sm.run_len[p][d] : 0u;
+        if (run_len != 0) {
+            const uint32_t run_g = sm.run_g[p][d];
+            const K* sp = sm.keys + sm.run_slot[p][d];
+            K* gp = dst + run_g;
+            uint32_t head = (kVec - ((run_g + mis) & (kVec - 1))) & (kVec - 1);
+            head = head < run_len ? head : run_len;
+            const uint32_t body = (run_len - head) & ~(kVec - 1);
+            if (copier && body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
+            if (!copier || !kSplit) {
+                for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
+                for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+            }
+        }
+    };
+    int par = 0;             // parity of the tile being counted / ranked
+    bool have_prev = false;  // LATE_WRITE: a staged tile (parity par ^ 1) still waits for its write-out
     bool hot_prev = false;  // the count guesses from this CTA's previous tile
     while (tile_len != 0) {
         ISORT_TTICK(q0);
@@ -128,9 +162,14 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
 
         // ---------------- one thread per digit: total, look-back, aligned run start, slot bases
         int nonzero = 0;
+#if ISORT_T_LATE_WRITE
+        if (tid >= kRadix && have_prev) write_out(par ^ 1);  // the previous tile's run edges
+#endif
         if (tid < kRadix) {
             ISORT_TTICK(qa);
+#if !ISORT_T_LATE_WRITE
             bulk_wait_read();  // the previous tile's copies have read the staging buffer
+#endif
             ISORT_TTICK(qb);
             const int d = tid;
             uint32_t tot = 0;
@@ -138,11 +177,18 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             for (int w = 0; w < kWarps; ++w) tot += sm.cnt[w][d];
             nonzero = tot != 0;
             ISORT_TTICK(qd);
+#if ISORT_T_LATE_WRITE
+            // the previous tile leaves between this tile's publication and its walk: the
+            // copies are issued while the predecessors this walk needs are still publishing
+            if (tile == 0) st_relaxed_gpu(&lb[d], LT::kInc | tot);
+            else st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kAgg | tot);
+            if (have_prev) write_out(par ^ 1);
+#endif
             uint32_t excl = 0;
             if (tile == 0) {
-                st_relaxed_gpu(&lb[d], LT::kInc | tot);
+                if (!ISORT_T_LATE_WRITE) st_relaxed_gpu(&lb[d], LT::kInc | tot);
             } else {
-                st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kAgg | tot);
+                if (!ISORT_T_LATE_WRITE) st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kAgg | tot);
 #ifdef ISORT_LB_STATS
                 unsigned long long lbst[3] = {0, 0, 0};
                 excl = lookback_digit<LW, kLookbackWindowT>(lb, static_cast<int>(tile) - 1, d, 0u, lbst);
@@ -158,6 +204,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 st_relaxed_gpu(&lb[static_cast<size_t>(tile) * kRadix + d], LT::kInc | (excl + tot));
             }
             ISORT_TTICK(qc);
+#if ISORT_T_LATE_WRITE
+            bulk_wait_read();  // the previous tile's copies have read the staging buffer
+#endif
             const uint32_t sc = warp_inclusive_scan(tot);
             if (lane == 31) sm.tot_w[warp] = sc;
             if (BLOCK == kRadix)
@@ -170,9 +219,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             const uint32_t run_g = sm.offs[d] + excl;
             uint32_t base = pre + sc - tot + kVec * static_cast<uint32_t>(d);
             base += (run_g + mis - base) & (kVec - 1);  // slot == global index + mis (mod kVec)
-            sm.run_slot[d] = base;
-            sm.run_len[d] = tot;
-            sm.run_g[d] = run_g;
+            sm.run_slot[par][d] = base;
+            sm.run_len[par][d] = tot;
+            sm.run_g[par][d] = run_g;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {  // per-warp slot bases for the rank
                 const uint32_t v = sm.cnt[w][d];
@@ -223,30 +272,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         };
         load_next();
 
-        // ---------------- write-out of digit d's run -> dst[run_g, run_g + run_len): thread d
-        // issues the bulk copy of its aligned interior, thread kRadix + d stores the keys
-        // around it (the same split inside every warp, or the write-out before the loads,
-        // measured no faster)
-        {
-            const int d = tid & (kRadix - 1);
-            const bool copier = tid < kRadix;
-            const bool active = tid < 2 * kRadix;
-            const uint32_t run_len = active ? sm.run_len[d] : 0u;
-            if (run_len != 0) {
-                const uint32_t run_g = sm.run_g[d];
-                const K* sp = sm.keys + sm.run_slot[d];
-                K* gp = dst + run_g;
-                uint32_t head = (kVec - ((run_g + mis) & (kVec - 1))) & (kVec - 1);
-                head = head < run_len ? head : run_len;
-                const uint32_t body = (run_len - head) & ~(kVec - 1);
-                if (copier) {
-                    if (body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
-                } else {
-                    for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
-                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
-                }
-            }
-        }
+#if !ISORT_T_LATE_WRITE
+        write_out(par);
+#endif
+        par ^= 1;
+        have_prev = true;
         tile = next;
         tile_len = next_len;
         ISORT_TTICK(q4);
@@ -266,6 +296,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         for (int i = 0; i < 8; ++i) atomicAdd(&st->prof[i], static_cast<unsigned long long>(acc[i]));
 #endif
 #undef ISORT_TTICK
+#if ISORT_T_LATE_WRITE
+    if (have_prev) write_out(par ^ 1);  // the last tile (staged before the loop's final barrier)
+#endif
     if (tid < kRadix) bulk_wait_all();  // this CTA's bulk stores complete before it exits
 }
 
