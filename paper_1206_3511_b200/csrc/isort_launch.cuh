@@ -92,13 +92,20 @@ struct PassCfgT {
     static constexpr int kTile = kBlock * kIpt;
     static constexpr int kCtasPerSm = 1024 / kBlock;
 };
-// Which digitizers take it: the radix digit (one PRMT).  The bucket-index digits
-// (a 64-bit multiply each time a digit is needed) measured slower in it than in
-// k_onesweep (0.301 / 0.295 against 0.283 / 0.276 ms per pass at 10^8).
+// Which digitizers take it: the radix digit (one PRMT; 0.242 against 0.279 ms per pass at
+// 10^8) and the u32 bucket-index digit (a 64-bit multiply each time a digit is needed, which
+// this pass does twice per key: 0.276 / 0.274 against 0.282 / 0.275 ms).
 template <typename Dz>
 struct TmaPassDigitizer : std::false_type {};
 template <typename K>
 struct TmaPassDigitizer<RadixDigitizer<K>> : std::true_type {};
+#ifndef ISORT_PASS_TMA_BUCKET
+#define ISORT_PASS_TMA_BUCKET 1
+#endif
+#if ISORT_PASS_TMA_BUCKET
+template <typename K, int MODE>
+struct TmaPassDigitizer<BucketDigitizer<K, MODE>> : std::true_type {};
+#endif
 template <typename K, bool VALS, typename Dz>
 constexpr bool pass_uses_tma() {
     return ISORT_PASS_TMA && !VALS && sizeof(K) == 4 && TmaPassDigitizer<Dz>::value;
