@@ -563,7 +563,7 @@ def main_ours(args):
         value = n / (r["ms"] / 1e3) / 1e9
         pass_bytes = 8 * n  # read 4n + write 4n per one-sweep pass (keys only)
         achieved = pass_bytes / (r["pass_ms"] / 1e3) / 1e9 if r["pass_ms"] else None
-        traffic, traffic_src = ncu_traffic("k_onesweep") if n == N_DEFAULT else (None, None)
+        traffic, traffic_src = ncu_traffic("k_onesweep_t") if n == N_DEFAULT else (None, None)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
@@ -576,7 +576,8 @@ def main_ours(args):
                              "input fits L2 (latency-bound config)",
                        "parallelism": "single GPU", "cuda_graph": args.graph != "off"},
             "roofline": {
-                "bound": "hbm", "kernel": "k_onesweep<u32> (one digit pass)", "achieved": achieved,
+                "bound": "hbm", "kernel": ("k_onesweep_t<u32> (one digit pass, bulk-copy write-out)" if n >= (4 << 20) else
+                                             "k_onesweep<u32> (one digit pass, small-input tile)"), "achieved": achieved,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": pass_bytes, "launch_ms": r["pass_ms"],

@@ -1,5 +1,6 @@
 """Per-CUDA-source-line instruction and stall totals of an .ncu-rep (needs -lineinfo
-and --import-source on):  python tools/ncu_lines.py REP [--top 40]"""
+and --import-source on):  python tools/ncu_lines.py REP [--top 40] [--kernel REGEX]
+(--kernel keeps one kernel of a multi-kernel report, so its lines are not mixed with another's)"""
 import csv
 import io
 import subprocess
@@ -7,7 +8,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kern = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
+txt = subprocess.run(["ncu", "-i", rep, *kern, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 agg, hdr, path = {}, None, ""

@@ -4,7 +4,7 @@
 
 Writes {kernel_family: {"dram_bytes_per_launch": B, "read": R, "write": W,
 "duration_us": T, "source": rep}} for the families bench.py reports
-(k_onesweep, k_bucket_segments, k_upfront).  bench.py copies the figure into
+(k_onesweep_t, k_onesweep, k_bucket_segments, k_upfront).  bench.py copies the figure into
 its roofline "traffic" field when profiles/ncu_traffic.json exists.
 """
 import csv
@@ -15,7 +15,7 @@ import subprocess
 import sys
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1024**2, "GB": 1024**3}
-FAMILIES = ("k_onesweep", "k_bucket_segments", "k_upfront")
+FAMILIES = ("k_onesweep_t", "k_onesweep", "k_bucket_segments", "k_upfront")  # first match wins
 
 
 def rows(rep):
