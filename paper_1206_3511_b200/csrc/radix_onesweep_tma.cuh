@@ -14,12 +14,16 @@
 //     run while the CTA already counts its next tile: nothing waits for it until
 //     the next tile's rank, a whole count phase and per-digit section later;
 //   * the aligned slots need the run's global position, so the look-back comes
-//     before the rank (k_onesweep walks after chunk 0 is staged);
+//     before the rank (k_onesweep walks after chunk 0 is staged).  A walk right
+//     after the publication mostly waits for the nearest predecessors to publish;
+//     so the PREVIOUS tile's write-out (the copies' issue and the edge stores) sits
+//     between this tile's publication and its walk (ISORT_T_LATE_WRITE): walk
+//     rounds that stop at an unpublished predecessor drop from 2.2 to 0.4 per tile;
 //   * the next tile's ticket is taken after the rank and its keys are loaded
-//     during the write-out.
+//     right after the barrier that ends the rank.
 // Per 32 keys this removes the second key read (1 L1 wavefront), the staged-key
 // load (1), the out_base lookup (~1.5) and most of the scattered STG (~2.5 ->
-// 0.6): 15.1 L1 wavefronts against 19.0, 0.265 ms against 0.279 ms per pass at
+// 0.6): 14.5 L1 wavefronts against 19.0, 0.242 ms against 0.279 ms per pass at
 // 10^8 keys (DESIGN.md section 3.1 has the phase split and what was tried).
 #pragma once
 
@@ -35,7 +39,7 @@ struct OnesweepTSmem {
     static constexpr int kStage = kTile + kVec * kRadix;           // <= kVec - 1 pad slots before each run (+ 1 spare)
     uint32_t cnt[kWarps][kRadix];  // counts; then per-warp slot bases
     uint32_t offs[kRadix];         // pass digit offsets (from K2)
-    uint32_t tot_w[kRadix / 32];
+    uint32_t tot_w[kWarps];
     uint32_t run_slot[2][kRadix];  // digit d's run (by tile parity): first staging slot,
     uint32_t run_len[2][kRadix];   // keys,
     uint32_t run_g[2][kRadix];     // and global index of its first key
@@ -51,6 +55,7 @@ struct OnesweepTSmem {
 #ifndef ISORT_T_LATE_WRITE
 #define ISORT_T_LATE_WRITE 1
 #endif
+
 #ifndef ISORT_T_LB_WINDOW
 #define ISORT_T_LB_WINDOW 4
 #endif
@@ -121,12 +126,8 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     // issues the bulk copy of its aligned interior, thread kRadix + d stores the keys
     // around it (the same split inside every warp, or the write-out before the loads,
     // measured no faster).
-    auto write_out = [&](int p) {
-        constexpr bool kSplit = BLOCK >= 2 * kRadix;  // else thread d does both
-        const int d = tid & (kRadix - 1);
-        const bool copier = tid < kRadix;
-        const bool active = tid < 2 * kRadix;
-        const uint32_t run_len = active ? sm.run_len[p][d] : 0u;
+    auto write_run = [&](int p, int d, bool copier, bool edges) {
+        const uint32_t run_len = sm.run_len[p][d];
         if (run_len != 0) {
             const uint32_t run_g = sm.run_g[p][d];
             const K* sp = sm.keys + sm.run_slot[p][d];
@@ -135,11 +136,15 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             head = head < run_len ? head : run_len;
             const uint32_t body = (run_len - head) & ~(kVec - 1);
             if (copier && body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
-            if (!copier || !kSplit) {
+            if (edges) {
                 for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
                 for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
             }
         }
+    };
+    auto write_out = [&](int p) {
+        constexpr bool kSplit = BLOCK >= 2 * kRadix;  // else thread d does both
+        if (tid < 2 * kRadix) write_run(p, tid & (kRadix - 1), tid < kRadix, tid >= kRadix || !kSplit);
     };
     int par = 0;             // parity of the tile being counted / ranked
     bool have_prev = false;  // LATE_WRITE: a staged tile (parity par ^ 1) still waits for its write-out
