@@ -85,10 +85,24 @@ struct PassCfg {
 #ifndef ISORT_PASS_BLOCK_T
 #define ISORT_PASS_BLOCK_T 512
 #endif
-template <typename K>
+#ifndef ISORT_PASS_IPT_TV
+#define ISORT_PASS_IPT_TV 16  // with a payload: 8,192-pair tiles (two staged arrays)
+#endif
+#ifndef ISORT_PASS_TMA_VALS
+#define ISORT_PASS_TMA_VALS 1
+#endif
+// With a payload the bulk-copy pass wins up to ~2 x 10^8 pairs and then loses to k_onesweep
+// (uniform keys, ms per 10^8 pairs at n = 1e8 / 2.5e8 / 5e8 / 1e9: 0.507 / 0.525 / 0.560 / 0.591
+// against 0.527 / 0.514 / 0.518 / 0.520; the keys-only pass does not degrade: 0.228 at 1e9), so
+// larger sorts with a payload keep k_onesweep.
+#ifndef ISORT_PASS_TMA_VALS_MAX_N
+#define ISORT_PASS_TMA_VALS_MAX_N 150000000ull
+#endif
+constexpr uint64_t kTmaValsMaxN = ISORT_PASS_TMA_VALS_MAX_N;
+template <typename K, bool VALS = false>
 struct PassCfgT {
     static constexpr int kBlock = ISORT_PASS_BLOCK_T;
-    static constexpr int kIpt = ISORT_PASS_IPT_T;
+    static constexpr int kIpt = VALS ? ISORT_PASS_IPT_TV : ISORT_PASS_IPT_T;
     static constexpr int kTile = kBlock * kIpt;
     static constexpr int kCtasPerSm = 1024 / kBlock;
 };
@@ -108,7 +122,7 @@ struct TmaPassDigitizer<BucketDigitizer<K, MODE>> : std::true_type {};
 #endif
 template <typename K, bool VALS, typename Dz>
 constexpr bool pass_uses_tma() {
-    return ISORT_PASS_TMA && !VALS && sizeof(K) == 4 && TmaPassDigitizer<Dz>::value;
+    return ISORT_PASS_TMA && (!VALS || ISORT_PASS_TMA_VALS) && sizeof(K) == 4 && TmaPassDigitizer<Dz>::value;
 }
 
 // Smallest tile any digit pass of a pipeline over n keys may use: it sizes the
@@ -118,7 +132,8 @@ template <typename K, bool VALS>
 inline int pass_tile(uint64_t n) {
     if (n < kSmallN) return PassCfg<K, VALS, 1>::kTile;
     const int t = PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
-    if (ISORT_PASS_TMA && !VALS && sizeof(K) == 4) return PassCfgT<K>::kTile < t ? PassCfgT<K>::kTile : t;
+    if (ISORT_PASS_TMA && (!VALS || ISORT_PASS_TMA_VALS) && sizeof(K) == 4)
+        return PassCfgT<K, VALS>::kTile < t ? PassCfgT<K, VALS>::kTile : t;
     return t;
 }
 // Tile of the partition (scatter) pass, which keeps the k_onesweep shapes.
@@ -173,9 +188,9 @@ template <typename K, bool VALS, typename Dz, typename Cfg, bool SCATTER = false
 void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
                    uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s,
                    const ScatterArg<SCATTER> scat = ScatterArg<SCATTER>{});
-template <typename K, typename Dz>
-void launch_passes_t(const K* kin, K* kout, K* kalt, uint64_t n, RadixState* st, void* lookback, uint32_t tiles,
-                     const Dz& dz, cudaStream_t s);
+template <typename K, bool VALS, typename Dz>
+void launch_passes_t(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
+                     uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s);
 template <typename K, typename Dz>
 int launch_histogram(const K* kin, uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz,
                      int plan_flags, bool zero_state, cudaStream_t s);
@@ -215,24 +230,25 @@ void launch_passes(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t
     }
 }
 
-// Keys-only passes with the bulk-copy write-out (k_onesweep_t), one launch per digit slot.
-template <typename K, typename Dz>
-void launch_passes_t(const K* kin, K* kout, K* kalt, uint64_t n, RadixState* st, void* lookback, uint32_t tiles,
-                     const Dz& dz, cudaStream_t s) {
+// Passes with the bulk-copy write-out (k_onesweep_t), one launch per digit slot.
+template <typename K, bool VALS, typename Dz>
+void launch_passes_t(const K* kin, K* kout, K* kalt, const uint32_t* vin, uint32_t* vout, uint32_t* valt, bool iota,
+                     uint64_t n, RadixState* st, void* lookback, uint32_t tiles, const Dz& dz, cudaStream_t s) {
     constexpr int D = Dz::kDigits;
-    using Cfg = PassCfgT<K>;
-    using Smem = OnesweepTSmem<K, Cfg::kBlock, Cfg::kIpt>;
+    using Cfg = PassCfgT<K, VALS>;
+    using Smem = OnesweepTSmem<K, Cfg::kBlock, Cfg::kIpt, VALS>;
     const bool fast = rank_fast_path_ok();
     const bool narrow = lb_word_bytes(n) == 4;
-    auto* kern = fast ? (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, false, uint32_t>
-                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, false, unsigned long long>)
-                      : (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, true, uint32_t>
-                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, true, unsigned long long>);
+    auto* kern = fast ? (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS, false, uint32_t>
+                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS, false, unsigned long long>)
+                      : (narrow ? k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS, true, uint32_t>
+                                : k_onesweep_t<K, Dz, Cfg::kBlock, Cfg::kIpt, VALS, true, unsigned long long>);
     set_max_smem_once(kern, sizeof(Smem));
     const unsigned cap = static_cast<unsigned>(Cfg::kCtasPerSm * sm_count());
     const unsigned grid3 = tiles < cap ? tiles : cap;
     for (int slot = 0; slot < D; ++slot) {
-        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, n, st, lookback, tiles, slot, dz);
+        kern<<<grid3, Cfg::kBlock, sizeof(Smem), s>>>(kin, kout, kalt, vin, vout, valt, iota ? 1 : 0, n, st, lookback,
+                                                        tiles, slot, dz);
         static const char* kPassNames[kMaxDigits] = {"pass0", "pass1", "pass2", "pass3",
                                                      "pass4", "pass5", "pass6", "pass7"};
         prof_mark(s, kPassNames[slot]);
@@ -291,8 +307,10 @@ int launch_radix_pipeline(const K* kin, K* kout, K* kalt, const uint32_t* vin, u
         using Cfg = PassCfg<K, VALS, 1>;
         launch_passes<K, VALS, Dz, Cfg>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles_of(Cfg::kTile),
                                         dz, s);
-    } else if constexpr (pass_uses_tma<K, VALS, Dz>()) {
-        launch_passes_t<K, Dz>(kin, kout, kalt, n, st, lookback, tiles_of(PassCfgT<K>::kTile), dz, s);
+    } else if (pass_uses_tma<K, VALS, Dz>() && (!VALS || n <= kTmaValsMaxN)) {
+        if constexpr (pass_uses_tma<K, VALS, Dz>())
+            launch_passes_t<K, VALS, Dz>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback,
+                                         tiles_of(PassCfgT<K, VALS>::kTile), dz, s);
     } else {
         using Cfg = PassCfg<K, VALS, ISORT_PASS_CHUNKS>;
         launch_passes<K, VALS, Dz, Cfg>(kin, kout, kalt, vin, vout, valt, iota, n, st, lookback, tiles_of(Cfg::kTile),

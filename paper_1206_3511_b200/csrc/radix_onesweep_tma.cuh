@@ -31,7 +31,7 @@
 
 namespace isort {
 
-template <typename K, int BLOCK, int IPT>
+template <typename K, int BLOCK, int IPT, bool VALS = false>
 struct OnesweepTSmem {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kTile = BLOCK * IPT;
@@ -45,6 +45,7 @@ struct OnesweepTSmem {
     uint32_t run_g[2][kRadix];     // and global index of its first key
     uint32_t tile_next;
     alignas(16) K keys[kStage];
+    alignas(16) uint32_t vals[VALS ? kStage : 4];  // the payload, staged at the key's slot
 };
 
 // Look-back window (predecessors read per round trip and digit).  The walk is spent
@@ -61,12 +62,15 @@ struct OnesweepTSmem {
 #endif
 constexpr int kLookbackWindowT = ISORT_T_LB_WINDOW;
 
-template <typename K, typename Dz, int BLOCK, int IPT, bool SAFE, typename LW>
+template <typename K, typename Dz, int BLOCK, int IPT, bool VALS, bool SAFE, typename LW>
 __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
-    k_onesweep_t(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt, uint64_t n,
-                 RadixState* __restrict__ st, void* __restrict__ lookback, uint32_t num_tiles, int slot, Dz dz) {
+    k_onesweep_t(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
+                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
+                 int iota_vals, uint64_t n, RadixState* __restrict__ st, void* __restrict__ lookback,
+                 uint32_t num_tiles, int slot, Dz dz) {
     using LT = LbTraits<LW>;
-    using Smem = OnesweepTSmem<K, BLOCK, IPT>;
+    using Smem = OnesweepTSmem<K, BLOCK, IPT, VALS>;
+    static_assert(!VALS || sizeof(K) == 4, "payload staging shares the key's 16-byte congruence: u32 keys");
     constexpr int kWarps = Smem::kWarps;
     constexpr int kTile = Smem::kTile;
     constexpr uint32_t kVec = Smem::kVec;
@@ -85,6 +89,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     // key index of dst[0] within its 16-byte block: staged slot == global index + mis (mod kVec)
     const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) / sizeof(K)) & (kVec - 1);
     const uint64_t pol = ISORT_POL_STREAM;
+    const uint32_t* vsrc = src_id == kBufIn ? vals_in : (src_id == kBufOut ? vals_out : vals_alt);
+    uint32_t* vdst = dst_id == kBufOut ? vals_out : vals_alt;
+    const bool gen_iota = VALS && iota_vals && slot == 0;  // the first executed pass generates positions
+    // the payload leaves by bulk copy too when its array shares the keys' 16-byte phase (else by plain stores)
+    const bool vbulk = VALS && ((reinterpret_cast<uintptr_t>(vdst) / 4) & 3u) == mis;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -108,11 +117,20 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     uint32_t tile = sm.tile_next;
     uint32_t tile_len = len_of(tile);
     K key[IPT];
-    {
-        const K* ws = src + static_cast<uint64_t>(tile) * kTile + wofs;
+    uint32_t val[VALS ? IPT : 1];
+    auto load_tile = [&](uint32_t t, uint32_t len) {  // warp-striped: (item, lane) order = input order
+        const uint64_t tb = static_cast<uint64_t>(t < num_tiles ? t : 0u) * kTile;
+        const K* ws = src + tb + wofs;
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) key[i] = wofs + i * 32u < tile_len ? ldg_hint(ws + i * 32, pol) : static_cast<K>(0);
-    }
+        for (int i = 0; i < IPT; ++i) key[i] = wofs + i * 32u < len ? ldg_hint(ws + i * 32, pol) : static_cast<K>(0);
+        if constexpr (VALS) {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i)
+                val[i] = gen_iota ? static_cast<uint32_t>(tb + wofs + i * 32u)
+                                  : (wofs + i * 32u < len ? ldg_stream(vsrc + tb + wofs + i * 32u) : 0u);
+        }
+    };
+    load_tile(tile, tile_len);
 
 #ifdef ISORT_PHASE_TIMING
     long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -139,6 +157,19 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             if (edges) {
                 for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
                 for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+            }
+            if constexpr (VALS) {
+                const uint32_t* vp = sm.vals + sm.run_slot[p][d];
+                uint32_t* vg = vdst + run_g;
+                if (vbulk) {
+                    if (copier && body) bulk_s2g(vg + head, vp + head, body * 4u);
+                    if (edges) {
+                        for (uint32_t i = 0; i < head; ++i) stg_hint(vg + i, vp[i], pol);
+                        for (uint32_t i = head + body; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
+                    }
+                } else if (edges) {
+                    for (uint32_t i = 0; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
+                }
             }
         }
     };
@@ -245,6 +276,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
             for (int i = 0; i < IPT; ++i) {
                 const uint32_t s = warp_slot_agg<SAFE>(wc, dz.digit_sh(key[i], dsh), agg);
                 sm.keys[s] = key[i];
+                if constexpr (VALS) sm.vals[s] = val[i];
             }
         } else {
 #pragma unroll
@@ -252,6 +284,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
                 if (full || wofs + i * 32u < tile_len) {
                     const uint32_t s = warp_slot<SAFE>(wc, dz.digit_sh(key[i], dsh));
                     sm.keys[s] = key[i];
+                    if constexpr (VALS) sm.vals[s] = val[i];
                 }
             }
         }
@@ -269,13 +302,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         ISORT_TTICK(q3);
         const uint32_t next = sm.tile_next;
         const uint32_t next_len = len_of(next);
-        auto load_next = [&]() {  // the next tile's keys: in flight during the write-out
-            const K* ns = src + static_cast<uint64_t>(next < num_tiles ? next : 0u) * kTile + wofs;
-#pragma unroll
-            for (int i = 0; i < IPT; ++i)
-                key[i] = wofs + i * 32u < next_len ? ldg_hint(ns + i * 32, pol) : static_cast<K>(0);
-        };
-        load_next();
+        load_tile(next, next_len);  // the next tile: in flight during the next count
 
 #if !ISORT_T_LATE_WRITE
         write_out(par);

@@ -59,14 +59,16 @@ def _assert_fast(sass_ops, f):
 
 def test_fast_rank_is_returning_shared_atomic(sass_ops):
     # the rank is a returning ATOMS.ADD; the counts are non-returning (ATOMS.POPC.INC.32 RZ / ATOMS.ADD RZ)
-    # k_onesweep_t<u32, RadixDigitizer<u32>, 512, 32, SAFE=0, LW>: keys-only passes over large inputs
-    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb0E"):
+    # k_onesweep_t<u32, RadixDigitizer<u32>, 512, 32, VALS=0, SAFE=0, LW>: keys-only passes over large inputs
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb0ELb0E"):
         _assert_fast(sass_ops, f)
-    # k_onesweep<u32, RadixDigitizer<u32>, 512, 12, 2, VALS=1, SAFE=0, SCATTER=0, LW>: passes with a payload
-    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi2ELb1ELb0ELb0E"):
+    # k_onesweep_t<u32, RadixDigitizer<u32>, 512, 16, VALS=1, SAFE=0, LW>: the same with a payload
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi16ELb1ELb0E"):
         _assert_fast(sass_ops, f)
-    # k_onesweep<u32, RadixDigitizer<u32>, 512, 16, 1, VALS=0, SAFE=0, SCATTER=0, LW>: small inputs
+    # k_onesweep<u32, RadixDigitizer<u32>, 512, IPT, 1, VALS, SAFE=0, SCATTER=0, LW>: small inputs
     for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi16ELi1ELb0ELb0ELb0E"):
+        _assert_fast(sass_ops, f)
+    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi1ELb1ELb0ELb0E"):
         _assert_fast(sass_ops, f)
 
 
@@ -78,9 +80,11 @@ def test_selftest_checks_the_same_instruction(sass_ops):
 
 
 def test_safe_rank_uses_match(sass_ops):
-    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb1E"):
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi32ELb0ELb1E"):
         assert sass_ops[f]["MATCH.ANY"] > 0, f
-    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi2ELb1ELb1ELb0E"):
+    for f in _find(sass_ops, "k_onesweep_tIj", "RadixDigitizerIj", "Li512ELi16ELb1ELb1E"):
+        assert sass_ops[f]["MATCH.ANY"] > 0, f
+    for f in _find(sass_ops, "k_onesweepIj", "RadixDigitizerIj", "Li512ELi12ELi1ELb1ELb1ELb0E"):
         assert sass_ops[f]["MATCH.ANY"] > 0, f
 
 
