@@ -104,7 +104,7 @@ struct PassCfgT {
     static constexpr int kBlock = ISORT_PASS_BLOCK_T;
     static constexpr int kIpt = VALS ? ISORT_PASS_IPT_TV : ISORT_PASS_IPT_T;
     static constexpr int kTile = kBlock * kIpt;
-    static constexpr int kCtasPerSm = 1024 / kBlock;
+    static constexpr int kCtasPerSm = ISORT_PASS_CTAS_T_OF(kBlock);
 };
 // Which digitizers take it: the radix digit (one PRMT; 0.242 against 0.279 ms per pass at
 // 10^8) and the u32 bucket-index digit (a 64-bit multiply each time a digit is needed, which

@@ -53,6 +53,11 @@ struct OnesweepTSmem {
 // takes ~8,400 of a tile's 27,400 cycles whatever the window (2 / 4 / 8 / 16 / 24:
 // 0.2623 / 0.2632 / 0.2652 / 0.274 / 0.28 ms per pass), and every round reads
 // window x 1 KB per tile from L2, so a narrow window is the cheaper one.
+#ifndef ISORT_PASS_CTAS_T  // resident CTAs per SM (the launch bound's minimum and the grid size)
+#define ISORT_PASS_CTAS_T_OF(block) (1024 / (block))
+#else
+#define ISORT_PASS_CTAS_T_OF(block) ISORT_PASS_CTAS_T
+#endif
 #ifndef ISORT_T_LATE_WRITE
 #define ISORT_T_LATE_WRITE 1
 #endif
@@ -63,7 +68,7 @@ struct OnesweepTSmem {
 constexpr int kLookbackWindowT = ISORT_T_LB_WINDOW;
 
 template <typename K, typename Dz, int BLOCK, int IPT, bool VALS, bool SAFE, typename LW>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+__global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
     k_onesweep_t(const K* __restrict__ keys_in, K* __restrict__ keys_out, K* __restrict__ keys_alt,
                  const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out, uint32_t* __restrict__ vals_alt,
                  int iota_vals, uint64_t n, RadixState* __restrict__ st, void* __restrict__ lookback,
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
     };
     auto write_out = [&](int p) {
         constexpr bool kSplit = BLOCK >= 2 * kRadix;  // else thread d does both
-        if (tid < 2 * kRadix) write_run(p, tid & (kRadix - 1), tid < kRadix, tid >= kRadix || !kSplit);
+        if (tid < (kSplit ? 2 * kRadix : kRadix)) write_run(p, tid & (kRadix - 1), tid < kRadix, tid >= kRadix || !kSplit);
     };
     int par = 0;             // parity of the tile being counted / ranked
     bool have_prev = false;  // LATE_WRITE: a staged tile (parity par ^ 1) still waits for its write-out
