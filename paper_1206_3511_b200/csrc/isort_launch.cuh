@@ -91,6 +91,18 @@ struct PassCfg {
 #ifndef ISORT_PASS_TMA_VALS
 #define ISORT_PASS_TMA_VALS 1
 #endif
+#ifndef ISORT_PASS_IPT_T64
+#define ISORT_PASS_IPT_T64 16  // u64 keys (keys only): 8,192-key tiles
+#endif
+#ifndef ISORT_PASS_IPT_T64V
+#define ISORT_PASS_IPT_T64V 12  // u64 keys with a payload: 6,144-pair tiles
+#endif
+#ifndef ISORT_PASS_TMA_U64
+#define ISORT_PASS_TMA_U64 1
+#endif
+#ifndef ISORT_PASS_TMA_U64V
+#define ISORT_PASS_TMA_U64V 1
+#endif
 // With a payload the bulk-copy pass wins up to ~2 x 10^8 pairs and then loses to k_onesweep
 // (uniform keys, ms per 10^8 pairs at n = 1e8 / 2.5e8 / 5e8 / 1e9: 0.507 / 0.525 / 0.560 / 0.591
 // against 0.527 / 0.514 / 0.518 / 0.520; the keys-only pass does not degrade: 0.228 at 1e9), so
@@ -102,7 +114,8 @@ constexpr uint64_t kTmaValsMaxN = ISORT_PASS_TMA_VALS_MAX_N;
 template <typename K, bool VALS = false>
 struct PassCfgT {
     static constexpr int kBlock = ISORT_PASS_BLOCK_T;
-    static constexpr int kIpt = VALS ? ISORT_PASS_IPT_TV : ISORT_PASS_IPT_T;
+    static constexpr int kIpt = sizeof(K) == 8 ? (VALS ? ISORT_PASS_IPT_T64V : ISORT_PASS_IPT_T64)
+                                               : (VALS ? ISORT_PASS_IPT_TV : ISORT_PASS_IPT_T);
     static constexpr int kTile = kBlock * kIpt;
     static constexpr int kCtasPerSm = ISORT_PASS_CTAS_T_OF(kBlock);
 };
@@ -118,11 +131,12 @@ struct TmaPassDigitizer<RadixDigitizer<K>> : std::true_type {};
 #endif
 #if ISORT_PASS_TMA_BUCKET
 template <typename K, int MODE>
-struct TmaPassDigitizer<BucketDigitizer<K, MODE>> : std::true_type {};
+struct TmaPassDigitizer<BucketDigitizer<K, MODE>> : std::integral_constant<bool, sizeof(K) == 4> {};
 #endif
 template <typename K, bool VALS, typename Dz>
 constexpr bool pass_uses_tma() {
-    return ISORT_PASS_TMA && (!VALS || ISORT_PASS_TMA_VALS) && sizeof(K) == 4 && TmaPassDigitizer<Dz>::value;
+    return ISORT_PASS_TMA && TmaPassDigitizer<Dz>::value &&
+           (sizeof(K) == 4 ? (!VALS || ISORT_PASS_TMA_VALS) : (VALS ? ISORT_PASS_TMA_U64V : ISORT_PASS_TMA_U64));
 }
 
 // Smallest tile any digit pass of a pipeline over n keys may use: it sizes the
@@ -132,7 +146,7 @@ template <typename K, bool VALS>
 inline int pass_tile(uint64_t n) {
     if (n < kSmallN) return PassCfg<K, VALS, 1>::kTile;
     const int t = PassCfg<K, VALS, ISORT_PASS_CHUNKS>::kTile;
-    if (ISORT_PASS_TMA && (!VALS || ISORT_PASS_TMA_VALS) && sizeof(K) == 4)
+    if (ISORT_PASS_TMA && (sizeof(K) == 4 ? (!VALS || ISORT_PASS_TMA_VALS) : (VALS ? ISORT_PASS_TMA_U64V : ISORT_PASS_TMA_U64)))
         return PassCfgT<K, VALS>::kTile < t ? PassCfgT<K, VALS>::kTile : t;
     return t;
 }

@@ -36,7 +36,8 @@ struct OnesweepTSmem {
     static constexpr int kWarps = BLOCK / 32;
     static constexpr int kTile = BLOCK * IPT;
     static constexpr int kVec = 16 / static_cast<int>(sizeof(K));  // keys per 16-byte block
-    static constexpr int kStage = kTile + kVec * kRadix;           // <= kVec - 1 pad slots before each run (+ 1 spare)
+    static constexpr int kSlotVec = VALS ? 4 : kVec;               // slots follow the global index modulo this
+    static constexpr int kStage = kTile + kSlotVec * kRadix;       // <= kSlotVec - 1 pad slots before each run (+ 1 spare)
     uint32_t cnt[kWarps][kRadix];  // counts; then per-warp slot bases
     uint32_t offs[kRadix];         // pass digit offsets (from K2)
     uint32_t tot_w[kWarps];
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
                  uint32_t num_tiles, int slot, Dz dz) {
     using LT = LbTraits<LW>;
     using Smem = OnesweepTSmem<K, BLOCK, IPT, VALS>;
-    static_assert(!VALS || sizeof(K) == 4, "payload staging shares the key's 16-byte congruence: u32 keys");
+
     constexpr int kWarps = Smem::kWarps;
     constexpr int kTile = Smem::kTile;
     constexpr uint32_t kVec = Smem::kVec;
@@ -91,14 +92,20 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
     K* dst = dst_id == kBufOut ? keys_out : keys_alt;
     const uint32_t dsh = dz.shift_for(pos);
     LW* lb = static_cast<LW*>(lookback) + static_cast<size_t>(slot) * num_tiles * kRadix;
-    // key index of dst[0] within its 16-byte block: staged slot == global index + mis (mod kVec)
-    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) / sizeof(K)) & (kVec - 1);
+    constexpr uint32_t kSlotVec = Smem::kSlotVec;
+    // A staged slot follows the global index: slot == index + mis (mod kSlotVec), mis = the element index of
+    // the output's first element within its 16-byte block.  Keys only: the key array's phase (2 or 4 keys per
+    // block).  With a payload: u32 keys use the key array's phase, u64 keys the payload array's (4 per block);
+    // the other array leaves by bulk copies too when its phase agrees, else by plain stores.
+    const uint32_t mis_k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) / sizeof(K)) & (kVec - 1);
     const uint64_t pol = ISORT_POL_STREAM;
     const uint32_t* vsrc = src_id == kBufIn ? vals_in : (src_id == kBufOut ? vals_out : vals_alt);
     uint32_t* vdst = dst_id == kBufOut ? vals_out : vals_alt;
     const bool gen_iota = VALS && iota_vals && slot == 0;  // the first executed pass generates positions
-    // the payload leaves by bulk copy too when its array shares the keys' 16-byte phase (else by plain stores)
-    const bool vbulk = VALS && ((reinterpret_cast<uintptr_t>(vdst) / 4) & 3u) == mis;
+    const uint32_t mis_v = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(vdst) / 4) & 3u;
+    const uint32_t mis = (VALS && sizeof(K) == 8) ? mis_v : mis_k;
+    const bool kbulk = !(VALS && sizeof(K) == 8) || ((mis_v ^ mis_k) & (kVec - 1)) == 0;
+    const bool vbulk = VALS && (sizeof(K) == 8 || mis_v == mis_k);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -155,25 +162,28 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
             const uint32_t run_g = sm.run_g[p][d];
             const K* sp = sm.keys + sm.run_slot[p][d];
             K* gp = dst + run_g;
-            uint32_t head = (kVec - ((run_g + mis) & (kVec - 1))) & (kVec - 1);
-            head = head < run_len ? head : run_len;
-            const uint32_t body = (run_len - head) & ~(kVec - 1);
-            if (copier && body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
-            if (edges) {
-                for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
-                for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+            {  // keys: head up to the first 16-byte boundary, bulk-copied interior, tail
+                uint32_t head = (kVec - ((run_g + mis_k) & (kVec - 1))) & (kVec - 1);
+                head = head < run_len ? head : run_len;
+                const uint32_t body = kbulk ? (run_len - head) & ~(kVec - 1) : 0u;
+                if (!kbulk) head = 0;
+                if (copier && body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
+                if (edges) {
+                    for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
+                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+                }
             }
             if constexpr (VALS) {
                 const uint32_t* vp = sm.vals + sm.run_slot[p][d];
                 uint32_t* vg = vdst + run_g;
-                if (vbulk) {
-                    if (copier && body) bulk_s2g(vg + head, vp + head, body * 4u);
-                    if (edges) {
-                        for (uint32_t i = 0; i < head; ++i) stg_hint(vg + i, vp[i], pol);
-                        for (uint32_t i = head + body; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
-                    }
-                } else if (edges) {
-                    for (uint32_t i = 0; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
+                uint32_t head = (4u - ((run_g + mis_v) & 3u)) & 3u;
+                head = head < run_len ? head : run_len;
+                const uint32_t body = vbulk ? (run_len - head) & ~3u : 0u;
+                if (!vbulk) head = 0;
+                if (copier && body) bulk_s2g(vg + head, vp + head, body * 4u);
+                if (edges) {
+                    for (uint32_t i = 0; i < head; ++i) stg_hint(vg + i, vp[i], pol);
+                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
                 }
             }
         }
@@ -258,8 +268,8 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
 #pragma unroll
             for (int w = 0; w < kRadix / 32; ++w) pre += w < warp ? sm.tot_w[w] : 0u;
             const uint32_t run_g = sm.offs[d] + excl;
-            uint32_t base = pre + sc - tot + kVec * static_cast<uint32_t>(d);
-            base += (run_g + mis - base) & (kVec - 1);  // slot == global index + mis (mod kVec)
+            uint32_t base = pre + sc - tot + kSlotVec * static_cast<uint32_t>(d);
+            base += (run_g + mis - base) & (kSlotVec - 1);  // slot == global index + mis (mod kSlotVec)
             sm.run_slot[par][d] = base;
             sm.run_len[par][d] = tot;
             sm.run_g[par][d] = run_g;

@@ -138,3 +138,61 @@ def test_tma_pass_loaded_payload(cuda, oracle):
     torch.cuda.synchronize()
     assert np.array_equal(kout.cpu().numpy().view(np.uint32), k[order])
     assert np.array_equal(vout.cpu().numpy().view(np.uint32), vals[order])
+
+
+@pytest.mark.parametrize("n", [KS, KS + 8191, KS + 8193, 5_000_011])
+@pytest.mark.parametrize("bits", [64, 40])
+def test_tma_pass_u64_keys(cuda, n, bits):
+    """u64 keys (keys only) take the pass with 8,192-key tiles and 16-byte blocks of two keys;
+    40-bit keys (the reference generator's range) skip the three trivial high passes."""
+    import torch
+
+    from paper_1206_3511_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(n % 1000 + bits)
+    k = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=n, dtype=np.uint64)
+    if bits < 64:
+        k >>= np.uint64(64 - bits)
+    kin = torch.from_numpy(k.view(np.int64).copy()).cuda()
+    for off in (0, 1):  # output on / 8 bytes off a 16-byte boundary
+        kout = torch.full((n + 2,), -1, dtype=torch.int64, device="cuda")
+        tb = lib.isort_radix_temp_bytes(n, 8, 0)
+        temp = torch.empty(tb, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.isort_radix_sort_u64(kin.data_ptr(), kout.data_ptr() + 8 * off, None, None, n, 0,
+                                            temp.data_ptr(), tb, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        got = kout.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got[off:off + n], np.sort(k)), (n, bits, off)
+        assert got[off + n] == np.uint64(0xFFFFFFFFFFFFFFFF) and (off == 0 or got[0] == np.uint64(0xFFFFFFFFFFFFFFFF))
+
+
+@pytest.mark.parametrize("n", [KS + 6143, KS + 6145, 5_000_011])
+@pytest.mark.parametrize("off_k,off_v", [(0, 0), (1, 2), (0, 1)])
+def test_tma_pass_u64_pairs(cuda, n, off_k, off_v):
+    """u64 keys with the position payload (6,144-pair tiles): slots follow the payload array's
+    16-byte phase; the key array leaves by bulk copies when its phase agrees modulo two keys
+    ((0, 0) and (1, 2)), by plain stores otherwise ((0, 1))."""
+    import torch
+
+    from paper_1206_3511_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(n % 977 + 3 * off_k + off_v)
+    k = rng.integers(0, 1 << 40, size=n, dtype=np.uint64)  # the reference generator's 40-bit keys, with duplicates
+    k[:: 97] = k[0]
+    order = np.argsort(k, kind="stable")
+    kin = torch.from_numpy(k.view(np.int64).copy()).cuda()
+    kout = torch.full((n + 2,), -1, dtype=torch.int64, device="cuda")
+    vout = torch.full((n + 4,), -1, dtype=torch.int32, device="cuda")
+    tb = lib.isort_radix_temp_bytes(n, 8, 1)
+    temp = torch.empty(tb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.isort_radix_sort_u64(kin.data_ptr(), kout.data_ptr() + 8 * off_k, None, vout.data_ptr() + 4 * off_v,
+                                        n, 2, temp.data_ptr(), tb, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    got = kout.cpu().numpy().view(np.uint64)
+    gv = vout.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got[off_k:off_k + n], k[order]), (n, off_k, off_v)
+    assert np.array_equal(gv[off_v:off_v + n], order.astype(np.uint32)), (n, off_k, off_v)
+    assert np.all(gv[:off_v] == U32_MAX) and np.all(gv[off_v + n:] == U32_MAX), "wrote outside vals_out"
+    assert got[off_k + n] == np.uint64(0xFFFFFFFFFFFFFFFF), "wrote outside keys_out"
