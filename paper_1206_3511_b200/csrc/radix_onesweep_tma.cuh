@@ -63,6 +63,13 @@ struct OnesweepTSmem {
 #define ISORT_T_LATE_WRITE 1
 #endif
 
+// Digitizers whose digit costs more than one instruction (the bucket index: a 64-bit multiply, a
+// 64-bit shift) compute it once, in the count, and keep it packed four to a register for the rank.
+#ifndef ISORT_T_DIGIT_CACHE
+#define ISORT_T_DIGIT_CACHE 1
+#endif
+template <typename Dz>
+struct CachesDigit : std::false_type {};
 #ifndef ISORT_T_LB_WINDOW
 #define ISORT_T_LB_WINDOW 4
 #endif
@@ -130,6 +137,15 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
     uint32_t tile_len = len_of(tile);
     K key[IPT];
     uint32_t val[VALS ? IPT : 1];
+    constexpr bool kCache = ISORT_T_DIGIT_CACHE && CachesDigit<Dz>::value && IPT % 4 == 0;
+    uint32_t dpk[kCache ? IPT / 4 : 1] = {};  // the tile's digits, four per register
+    auto put_digit = [&](int i, uint32_t d) {
+        if constexpr (kCache) dpk[i / 4] = (i % 4 == 0) ? d : (dpk[i / 4] | (d << (8 * (i % 4))));
+    };
+    auto get_digit = [&](int i, K k) -> uint32_t {
+        if constexpr (kCache) return (dpk[i / 4] >> (8 * (i % 4))) & 0xFFu;
+        return dz.digit_sh(k, dsh);
+    };
     auto load_tile = [&](uint32_t t, uint32_t len) {  // warp-striped: (item, lane) order = input order
         const uint64_t tb = static_cast<uint64_t>(t < num_tiles ? t : 0u) * kTile;
         const K* ws = src + tb + wofs;
@@ -202,11 +218,18 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
         if (full && hot_prev) {
             bool agg = true;
 #pragma unroll
-            for (int i = 0; i < IPT; ++i) count_digit_t<true>(wc, dz.digit_sh(key[i], dsh), agg);
+            for (int i = 0; i < IPT; ++i) {
+                const uint32_t d = dz.digit_sh(key[i], dsh);
+                put_digit(i, d);
+                count_digit_t<true>(wc, d, agg);
+            }
         } else {
 #pragma unroll
-            for (int i = 0; i < IPT; ++i)
-                if (full || wofs + i * 32u < tile_len) atomicAdd(&wc[dz.digit_sh(key[i], dsh)], 1u);
+            for (int i = 0; i < IPT; ++i) {
+                const uint32_t d = dz.digit_sh(key[i], dsh);
+                put_digit(i, d);
+                if (full || wofs + i * 32u < tile_len) atomicAdd(&wc[d], 1u);
+            }
         }
         __syncthreads();
         ISORT_TTICK(q1);
@@ -289,7 +312,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
             bool agg = true;
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-                const uint32_t s = warp_slot_agg<SAFE>(wc, dz.digit_sh(key[i], dsh), agg);
+                const uint32_t s = warp_slot_agg<SAFE>(wc, get_digit(i, key[i]), agg);
                 sm.keys[s] = key[i];
                 if constexpr (VALS) sm.vals[s] = val[i];
             }
@@ -297,7 +320,7 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 if (full || wofs + i * 32u < tile_len) {
-                    const uint32_t s = warp_slot<SAFE>(wc, dz.digit_sh(key[i], dsh));
+                    const uint32_t s = warp_slot<SAFE>(wc, get_digit(i, key[i]));
                     sm.keys[s] = key[i];
                     if constexpr (VALS) sm.vals[s] = val[i];
                 }
