@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
     // the other array leaves by bulk copies too when its phase agrees, else by plain stores.
     const uint32_t mis_k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) / sizeof(K)) & (kVec - 1);
     const uint64_t pol = ISORT_POL_STREAM;
+#ifndef ISORT_T_POL_EDGE
+#define ISORT_T_POL_EDGE pol
+#endif
+    const uint64_t pol_edge = ISORT_T_POL_EDGE;  // the run-edge stores (partial sectors their neighbours complete)
     const uint32_t* vsrc = src_id == kBufIn ? vals_in : (src_id == kBufOut ? vals_out : vals_alt);
     uint32_t* vdst = dst_id == kBufOut ? vals_out : vals_alt;
     const bool gen_iota = VALS && iota_vals && slot == 0;  // the first executed pass generates positions
@@ -185,8 +189,8 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
                 if (!kbulk) head = 0;
                 if (copier && body) bulk_s2g(gp + head, sp + head, body * static_cast<uint32_t>(sizeof(K)));
                 if (edges) {
-                    for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol);
-                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol);
+                    for (uint32_t i = 0; i < head; ++i) stg_hint(gp + i, sp[i], pol_edge);
+                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(gp + i, sp[i], pol_edge);
                 }
             }
             if constexpr (VALS) {
@@ -198,8 +202,8 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
                 if (!vbulk) head = 0;
                 if (copier && body) bulk_s2g(vg + head, vp + head, body * 4u);
                 if (edges) {
-                    for (uint32_t i = 0; i < head; ++i) stg_hint(vg + i, vp[i], pol);
-                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(vg + i, vp[i], pol);
+                    for (uint32_t i = 0; i < head; ++i) stg_hint(vg + i, vp[i], pol_edge);
+                    for (uint32_t i = head + body; i < run_len; ++i) stg_hint(vg + i, vp[i], pol_edge);
                 }
             }
         }
