@@ -153,6 +153,20 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
     auto load_tile = [&](uint32_t t, uint32_t len) {  // warp-striped: (item, lane) order = input order
         const uint64_t tb = static_cast<uint64_t>(t < num_tiles ? t : 0u) * kTile;
         const K* ws = src + tb + wofs;
+        if (len == static_cast<uint32_t>(kTile)) {  // a whole tile: no per-key bounds
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) key[i] = ldg_hint(ws + i * 32, pol);
+            if constexpr (VALS) {
+                if (gen_iota) {
+#pragma unroll
+                    for (int i = 0; i < IPT; ++i) val[i] = static_cast<uint32_t>(tb + wofs + i * 32u);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < IPT; ++i) val[i] = ldg_stream(vsrc + tb + wofs + i * 32u);
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < IPT; ++i) key[i] = wofs + i * 32u < len ? ldg_hint(ws + i * 32, pol) : static_cast<K>(0);
         if constexpr (VALS) {
@@ -227,12 +241,19 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
                 put_digit(i, d);
                 count_digit_t<true>(wc, d, agg);
             }
+        } else if (full) {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const uint32_t d = dz.digit_sh(key[i], dsh);
+                put_digit(i, d);
+                atomicAdd(&wc[d], 1u);
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 const uint32_t d = dz.digit_sh(key[i], dsh);
                 put_digit(i, d);
-                if (full || wofs + i * 32u < tile_len) atomicAdd(&wc[d], 1u);
+                if (wofs + i * 32u < tile_len) atomicAdd(&wc[d], 1u);
             }
         }
         __syncthreads();
@@ -320,10 +341,17 @@ __global__ void __launch_bounds__(BLOCK, ISORT_PASS_CTAS_T_OF(BLOCK))
                 sm.keys[s] = key[i];
                 if constexpr (VALS) sm.vals[s] = val[i];
             }
+        } else if (full) {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const uint32_t s = warp_slot<SAFE>(wc, get_digit(i, key[i]));
+                sm.keys[s] = key[i];
+                if constexpr (VALS) sm.vals[s] = val[i];
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-                if (full || wofs + i * 32u < tile_len) {
+                if (wofs + i * 32u < tile_len) {
                     const uint32_t s = warp_slot<SAFE>(wc, get_digit(i, key[i]));
                     sm.keys[s] = key[i];
                     if constexpr (VALS) sm.vals[s] = val[i];
